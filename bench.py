@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Benchmark: DP cell-transitions/s and solve time at L=1000, S=4000 (BASELINE.json).
+
+One "step" = one complete solve of the hot path:
+discretise + limits + leaf + all diagonals + Algorithm-2 reconstruction, on
+the config-4 chain (L=1000, S=4000, M = 0.25 * budget_ref), with the chain
+already resident in HBM.  `value` = nominal transitions of all ranks' solves
+per second (sum_{d=1}^{L} (n-d)(d+1)(S+1) = 6.708e11 per table), time = max
+over ranks of the CUDA-event time of K steps.
+
+N > 1: one process per GPU; rank r solves its own table at limit factor
+f_r = 0.25 + 0.05 r (the paper's multi-limit sweep) — independent
+units, no data-path collective, weak scaling.
+
+`--impl reference`: the oracle (oracle/, plain C, single thread) timed on the
+host on a bounded sample of the same workload (stages 1..150 of the config-4
+chain at S=4000), same metric.
+
+Launch: python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+        torchrun --nproc-per-node N bench.py --gpus N ...
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DP cell-transitions/sec and solve time (L=1000, 4000 slots); % HBM roofline"
+UNIT = "transitions/s"
+REF_WINDOW = 150  # stages in the oracle's bounded sample (reference arm steps)
+CPU_BASELINE_WINDOW = 180  # stages in the cpu_baseline sample (~10-20 s single-thread)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kernel", default=os.environ.get("ROTOR_KERNEL", "auto"))
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def n_transitions(L, S):
+    n = L + 1
+    return float(sum((n - d) * (d + 1) * (S + 1) for d in range(1, L + 1)))
+
+
+def alg_bytes_wavefront(L, S):
+    """Algorithmic HBM bytes of a diagonal-synchronous wavefront:
+    per diagonal d and slab l < d, the distinct rows |[1,n-d] U [d-l+1,n-l]| of
+    S+1 doubles are read once; every cell row is written once (8 B per value)."""
+    n = L + 1
+    rows = 0
+    for d in range(1, L + 1):
+        for l in range(d):
+            a0, a1 = 1, n - d
+            b0, b1 = d - l + 1, n - l
+            inter = max(0, min(a1, b1) - max(a0, b0) + 1)
+            rows += (a1 - a0 + 1) + (b1 - b0 + 1) - inter
+    cells = n * (n + 1) // 2
+    return 8.0 * (S + 1) * (rows + cells)
+
+
+# ----------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md)
+# ----------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def ncu_traffic(kernel_tag: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            js = json.load(f)
+        ent = js.get(kernel_tag)
+        return None if ent is None else ent.get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------
+# reference arm: the oracle on the host
+# ----------------------------------------------------------------------------
+def oracle_sample(window: int):
+    import chaingen as G
+    import oracle as O
+
+    p = G.config4()
+    t0 = time.perf_counter()
+    O.OracleSolve(p.chain, p.mem_limit, p.slots, window=(1, window))
+    dt = time.perf_counter() - t0
+    return n_transitions(window - 1, p.slots), dt
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle as O
+
+    O.build()
+    for _ in range(args.warmup):
+        oracle_sample(REF_WINDOW)
+    tot_tr, tot_t = 0.0, 0.0
+    for _ in range(args.steps):
+        tr, dt = oracle_sample(REF_WINDOW)
+        tot_tr += tr
+        tot_t += dt
+    v = tot_tr / tot_t
+    sample = (f"oracle fill of stages 1..{REF_WINDOW} of the config-4 chain (L=1000) at S=4000, "
+              f"{tot_tr / args.steps:.3e} transitions per step, single thread")
+    out = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg4_long_L1000_S4000 (bounded sample)", "L": REF_WINDOW - 1, "S": 4000},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------
+# our arm
+# ----------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import chaingen as G
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+        pg = dist
+    import __graft_entry__ as ge
+
+    if rank == 0:
+        ge.build_library()
+    if pg:
+        pg.barrier()
+    import paper_1911_13214_b200 as R
+
+    f = 0.25 + 0.05 * rank
+    cfg = {4: lambda: G.config4(f), 3: G.config3, 2: G.config2, 1: G.config1}[args.config]
+    p = cfg()
+    ch, L, S, M = p.chain, p.chain.L, p.slots, p.mem_limit
+    kernel = args.kernel
+    opts = dict(kernel=kernel, profile=True)
+
+    # device-resident inputs (the chain) and workspace
+    d_chain = {k: torch.from_numpy(np.asarray(getattr(ch, k)).astype(np.float64 if k in ("uf", "ub") else np.int64)).to(dev)
+               for k in ("uf", "ub", "wx", "wbx", "wy", "of", "ob")}
+    ws = torch.empty(R.workspace_bytes(L, S, **opts), dtype=torch.uint8, device=dev)
+    cap = R.max_ops(L)
+    out = dict(cost=torch.empty(1, dtype=torch.float64, device=dev),
+               ops=torch.empty((cap, 2), dtype=torch.int32, device=dev),
+               n_ops=torch.empty(1, dtype=torch.int64, device=dev),
+               status=torch.empty(1, dtype=torch.int32, device=dev))
+    stream = torch.cuda.current_stream()
+
+    def step():
+        R.solve_device(d_chain, L, M, S, ws, out, stream=stream, **opts)
+        return R.last_timings() if False else None
+
+    for _ in range(max(args.warmup, 0)):
+        step()
+    torch.cuda.synchronize()
+    st = int(out["status"].item())
+    if st != R.OK:
+        raise SystemExit(f"rank {rank}: solve status {R.STATUS.get(st)}")
+
+    clocks = ClockSampler(local)
+    fill_ms = []
+    total_launches = 0
+    fill_launches = 0
+    if pg:
+        pg.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        R.solve_device(d_chain, L, M, S, ws, out, stream=stream, **opts)
+        t = R.last_timings()  # syncs on this step's last event (phase events on the launch stream)
+        fill_ms.append(t["fill_ms"])
+        total_launches += t["total_launches"]
+        fill_launches = t["fill_launches"]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if pg:
+        pg.barrier()
+    clk = clocks.stop()
+    elapsed_ms = e0.elapsed_time(e1)
+    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if pg:
+        pg.all_reduce(tmax, op=pg.ReduceOp.MAX)
+    elapsed_ms = float(tmax.item())
+    cost = float(out["cost"].item())
+    n_ops = int(out["n_ops"].item())
+
+    # end-to-end through the public API with HOST buffers (H2D chain, D2H cost + ops inside)
+    e2e = None
+    if not args.no_e2e:
+        for _ in range(1):
+            R.solve(ch, M, S, workspace=ws, stream=stream, kernel=kernel)
+        torch.cuda.synchronize()
+        if pg:
+            pg.barrier()
+        t0 = time.perf_counter()
+        res = None
+        for _ in range(args.steps):
+            res = R.solve(ch, M, S, workspace=ws, stream=stream, kernel=kernel)
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        if pg:
+            pg.all_reduce(te, op=pg.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        assert res.cost == cost
+        h2d = sum(np.asarray(getattr(ch, k)).nbytes for k in ("uf", "ub", "wx", "wbx", "wy", "of", "ob"))
+        d2h = 8 + 8 + 4 + res.n_ops * 8
+        e2e = {"value": world * n_transitions(L, S) * args.steps / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": 1e3 * e2e_s / args.steps}
+
+    if pg:
+        pg.barrier()
+    if rank != 0:
+        if pg:
+            pg.destroy_process_group()
+        return 0
+
+    tr = n_transitions(L, S)
+    value = world * tr * args.steps / (elapsed_ms / 1e3)
+    peaks, peak_kind = measured_peaks()
+    fill_avg_ms = sum(fill_ms) / len(fill_ms)
+    use_tiled = kernel == "tiled"
+    if use_tiled:
+        roof = None  # filled by the tiled model below
+    b_alg = alg_bytes_wavefront(L, S)
+    achieved = b_alg / (fill_avg_ms / 1e3) / 1e9  # GB/s, fill phase = all K2 launches
+    peak = float(peaks["hbm_gbs"])
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": ncu_traffic("k_diag_wavefront"), "kernel": "k_diag_wavefront (all diagonals d=1..L)",
+                "alg_bytes_per_step": b_alg, "launches_per_step": fill_launches, "peak_source": peak_kind,
+                "fill_ms_per_step": fill_avg_ms}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        import oracle as O
+
+        O.build()
+        trc, dtc = oracle_sample(CPU_BASELINE_WINDOW)
+        cpu = {"value": trc / dtc, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"oracle fill of stages 1..{CPU_BASELINE_WINDOW} of the config-4 chain at S=4000 "
+                         f"({trc:.3e} transitions, {dtc:.1f} s, single thread, host {os.cpu_count()} cores)"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": p.name, "L": L, "S": S, "mem_limit_bytes": M, "limit_factor": 0.25,
+                   "kernel": kernel, "parallelism": f"independent tables x{world}",
+                   "l2": f"table {R.workspace_bytes(L, S) / 1e9:.1f} GB >> 126 MB L2 (no flush needed)"},
+        "solve_ms": elapsed_ms / args.steps, "fill_ms": fill_avg_ms, "transitions_per_table": tr,
+        "cost": cost, "n_ops": n_ops,
+        "clocks": clk, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": total_launches,
+    }
+    print(json.dumps(line), flush=True)
+    if pg:
+        pg.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,197 @@
+/*
+ * rotor.h — C ABI of the B200 (sm_100a) solver for the optimal persistent
+ * checkpointing DP of arXiv 1911.13214 ("Rotor").
+ *
+ * The library computes, on the GPU, the table C(s,t,m) of Theorem 1
+ * (PAPER.md P:717-739): the optimal time to process stages s..t of a chain
+ * within m memory slots, assuming a^{s-1} and delta^t are stored and a^{s-1}
+ * is not counted in m.  It then reconstructs the optimal operation
+ * sequence with Algorithm 2.  Sizes are discretised into S slots
+ * of M/S bytes, each rounded up (§5.2).  The readings of the paper
+ * it implements (fill order, tie rule, fp64 association, …) are listed in
+ * DESIGN.md §3; they are part of this contract.
+ *
+ * Conventions for every entry point
+ *   - Plain C types only; no exception or C++ type crosses the boundary.
+ *   - All output buffers are caller-owned.  Input buffers are read-only and
+ *     only read during the call (or, for the *_device variants, until the
+ *     work enqueued on `stream` completes).
+ *   - A `stream` argument is a cudaStream_t passed as void*; NULL means the
+ *     legacy default stream.  Device pointers must belong to the current
+ *     device of the calling thread.
+ *   - Every function returns a rotor_status.  On error, rotor_last_error()
+ *     returns a thread-local message.  Calls are thread-compatible, not
+ *     re-entrant on the same workspace.
+ */
+#ifndef ROTOR_H
+#define ROTOR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------------------
+ * The chain (§3.1; Table 1).
+ * n = L+1 stages; stage L+1 is the loss.  Arrays are 0-based
+ * storage of the paper's 1-based indices:
+ *   uf[l-1], ub[l-1]  time of F^l / B^l, l = 1..L+1        (finite, >= 0)
+ *   wx[l]             size of a^l, l = 0..L                 (bytes)
+ *   wbx[l-1]          size of abar^l, l = 1..L+1            (bytes)
+ *   wy[l]             size of delta^l, l = 0..L+1 (L+2 values)
+ *   of[l-1], ob[l-1]  memory overhead of F^l / B^l           (bytes)
+ * Host pointers for rotor_solve / rotor_solve_ex / rotor_solve_batch; device
+ * pointers for rotor_solve_device.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+    const double *uf, *ub;
+    const uint64_t *wx;
+    const uint64_t *wbx;
+    const uint64_t *wy;
+    const uint64_t *of, *ob;
+} rotor_chain;
+
+/* Schedule operations (Table 1): F_all, F_ck, F_null, B. */
+typedef enum { ROTOR_FALL = 0, ROTOR_FCK = 1, ROTOR_FNULL = 2, ROTOR_BWD = 3 } rotor_opcode;
+typedef struct {
+    int32_t op;    /* rotor_opcode */
+    int32_t stage; /* 1..L+1 */
+} rotor_op;
+
+typedef enum {
+    ROTOR_OK = 0,
+    ROTOR_EINPUT = 1,      /* bad argument: L < 1, S < 1, M = 0, NaN/negative time, NULL array */
+    ROTOR_INFEASIBLE = 2,  /* no valid persistent schedule within M: cost = +inf, n_ops = 0 */
+    ROTOR_EINVALID = 3,    /* internal consistency failure (reconstruction could not follow C) */
+    ROTOR_EDEVICE = 4,     /* CUDA error (message in rotor_last_error) */
+    ROTOR_ENOMEM = 5,      /* workspace too small / device allocation failed */
+    ROTOR_ETRUNC = 6       /* cost valid; ops truncated to ops_cap (n_ops holds the full count) */
+} rotor_status;
+
+/* Fill kernels. */
+typedef enum {
+    ROTOR_KERNEL_AUTO = 0,
+    ROTOR_KERNEL_WAVEFRONT = 1, /* one launch per diagonal d, one thread per (s,m) cell, k-loop */
+    ROTOR_KERNEL_TILED = 2      /* blocked (s,t)-tile min-plus evaluation (fast path) */
+} rotor_kernel;
+
+typedef struct {
+    int32_t restricted;  /* 1: F_all only at s = t — the paper's "revolve" baseline */
+    int32_t kernel;      /* rotor_kernel */
+    int32_t keep_argmin; /* 1: record D (uint16 argmin) during the fill (wavefront kernel only) */
+    int32_t profile;     /* 1: time the phases with CUDA events (see rotor_last_timings) */
+    int32_t reserved[4];
+} rotor_options;
+
+/* Default options: all zero (unrestricted, auto kernel, no D, no profiling). */
+
+/* ---------------------------------------------------------------------------
+ * rotor_solve — Algorithm 1 + Algorithm 2 for one chain and one memory limit.
+ *   chain, L   : host chain (above), L >= 1
+ *   mem_limit  : M in bytes (> 0); slots: S >= 1 (the paper uses 500)
+ *   cost_out   : C[1, L+1, S - slots(wx[0])] (Alg. 1 return); +inf when infeasible
+ *   ops        : caller buffer of ops_cap entries, or NULL for a size query
+ *   n_ops_out  : number of ops of the optimal sequence (written even when truncated)
+ * Uses a library-owned, per-device cached workspace and the legacy stream;
+ * blocks until the result is on the host.
+ * Returns ROTOR_OK, ROTOR_INFEASIBLE, ROTOR_ETRUNC or an error.
+ * ------------------------------------------------------------------------- */
+int rotor_solve(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int32_t slots, double *cost_out,
+                rotor_op *ops, int64_t ops_cap, int64_t *n_ops_out);
+
+/* rotor_solve with options, an explicit stream and optionally a caller-owned
+ * device workspace (e.g. torch-allocated) of workspace_bytes >=
+ * rotor_workspace_bytes(); d_workspace == NULL uses the library cache.
+ * Copies the (host) chain to the device and the cost/ops back inside the call
+ * (the end-to-end path); blocks until done. */
+int rotor_solve_ex(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int32_t slots,
+                   const rotor_options *opt, void *d_workspace, uint64_t workspace_bytes, void *stream,
+                   double *cost_out, rotor_op *ops, int64_t ops_cap, int64_t *n_ops_out);
+
+/* Device-resident solve: d_chain holds DEVICE pointers; results are written to
+ * device memory: *d_cost (double), d_ops[0..ops_cap), *d_n_ops (int64: op
+ * count, -1 if infeasible), *d_status (int32 rotor_status of the device
+ * phase).  Fully asynchronous on `stream` (no host synchronisation); host-side
+ * argument errors are returned immediately.  d_workspace is required. */
+int rotor_solve_device(const rotor_chain *d_chain, int32_t L, uint64_t mem_limit, int32_t slots,
+                       const rotor_options *opt, void *d_workspace, uint64_t workspace_bytes, void *stream,
+                       double *d_cost, rotor_op *d_ops, int64_t ops_cap, int64_t *d_n_ops, int32_t *d_status);
+
+/* Device workspace bytes needed for (L, S, options). */
+int rotor_workspace_bytes(int32_t L, int32_t slots, const rotor_options *opt, uint64_t *bytes);
+
+/* Upper bound on the op count of any schedule Algorithm 2 can return for L:
+ * n(n+1)/2 forwards + n backwards, n = L+1 (a node (s,t) split at s' emits
+ * s'-s forwards; by induction an interval of len stages emits at most
+ * len(len+1)/2) — a safe ops_cap. */
+int64_t rotor_max_ops(int32_t L);
+
+/* ---------------------------------------------------------------------------
+ * Batched multi-limit solve ("Algorithm 1 for 10 different memory
+ * limits"): n_chains chains x n_limits limits, each pair its own table with
+ * slot size limits[i*n_limits+j]/S (§5.2).  Runs on the current device.
+ *   chains[i], Ls[i]          : host chains
+ *   limits[i*n_limits + j]    : bytes
+ *   costs[i*n_limits + j]     : out
+ *   ops + ops_offsets[p]      : out, problem p = i*n_limits + j writes at most ops_caps[p]
+ *                               ops at ops + ops_offsets[p] (ops may be NULL: costs only)
+ *   n_ops[p]                  : out (-1 if infeasible); may be NULL
+ *   status[p]                 : out rotor_status per problem; may be NULL
+ * Returns ROTOR_OK if every problem ran (individual infeasibility is reported
+ * in status[]), else the first error.
+ * ------------------------------------------------------------------------- */
+int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_chains, const uint64_t *limits,
+                      int32_t n_limits, int32_t slots, const rotor_options *opt, void *stream, double *costs,
+                      rotor_op *ops, const int64_t *ops_offsets, const int64_t *ops_caps, int64_t *n_ops,
+                      int32_t *status);
+
+/* Longest-processing-time partition of n_items weighted items over n_parts
+ * parts (host helper for sharding independent solves across GPUs/ranks).
+ * part_of[i] in 0..n_parts-1; deterministic (ties -> lowest part index). */
+int rotor_partition_lpt(const double *weights, int32_t n_items, int32_t n_parts, int32_t *part_of);
+
+/* Nominal DP transitions of one table: sum_{d=1}^{L} (L+1-d)(d+1)(S+1)
+ * (every cell of diagonal d has d F_ck candidates + 1 F_all candidate). */
+double rotor_transitions(int32_t L, int32_t slots);
+
+/* ---------------------------------------------------------------------------
+ * Parity / debug: copy the tables of the LAST solve made by this thread
+ * (rotor_solve / rotor_solve_ex / rotor_solve_device) to host memory, in the
+ * canonical layout
+ *     cell(s,t) = d*n - d*(d-1)/2 + (s-1),  d = t-s, n = L+1
+ *     C_host[cell*(S+1) + m], m = 0..S      (fp64; +inf = infeasible)
+ *     D_host[cell*(S+1) + m]                (uint16: k = s'-s for an F_ck split,
+ *                                            0 for F_all / leaf, 0xFFFF if C = +inf)
+ * n_values must equal n(n+1)/2*(S+1).  Either pointer may be NULL.  D is
+ * derived on the device from C by Algorithm 2's test (smallest s' with
+ * C = C_ck) unless it was recorded during the fill.  The workspace of
+ * that solve must still be alive.  Synchronous.
+ * ------------------------------------------------------------------------- */
+int rotor_export_tables(double *C_host, uint16_t *D_host, int64_t n_values);
+
+/* Sampled export of the last solve: for r = 0..n_rows-1, copies the S+1 values
+ * C[s[r], t[r], 0..S] to C_host[r*(S+1) ...] (1 <= s[r] <= t[r] <= L+1).
+ * Used for parity at sizes whose full table does not fit host memory. */
+int rotor_export_rows(const int32_t *s, const int32_t *t, int64_t n_rows, double *C_host);
+
+/* Phase timings of the last solve on this thread (options.profile = 1). */
+typedef struct {
+    double pre_ms;         /* discretise + prefix sums + limits + leaf diagonal */
+    double fill_ms;        /* all diagonals d = 1..L (the dominant phase) */
+    double reconstruct_ms; /* Algorithm 2 walk */
+    int32_t fill_launches; /* kernels launched for the fill */
+    int32_t total_launches;/* kernels launched by the solve */
+} rotor_timings;
+int rotor_last_timings(rotor_timings *out);
+
+/* Release the library-owned cached workspaces (all devices). */
+int rotor_release(void);
+
+const char *rotor_last_error(void);
+int32_t rotor_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROTOR_H */

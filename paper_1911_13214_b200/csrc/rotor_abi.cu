@@ -1,0 +1,496 @@
+// Host side of the C ABI declared in include/rotor.h: argument validation,
+// workspace layout, launch sequencing, caching, export and timing.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "rotor.h"
+#include "rotor_common.cuh"
+#include "rotor_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                              \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) return fail(ROTOR_EDEVICE, "%s: %s", #x, cudaGetErrorString(e_)); \
+    } while (0)
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// Workspace layout of one problem (all offsets 256-byte aligned).
+struct Layout {
+    int L = 0, n = 0, S = 0;
+    int64_t pitch = 0, cells = 0;
+    int stack_cap = 0;
+    int64_t ops_cap = 0;
+    size_t off_wx, off_wbx, off_wy, off_of, off_ob, off_P, off_w, off_mnull, off_stack, off_res;
+    size_t off_chain, off_ops, off_C, off_D, off_tiled;
+    size_t total = 0;
+    bool has_D = false;
+};
+
+int64_t max_ops(int L) {
+    int64_t n = (int64_t)L + 1;
+    return n * (n + 1) / 2 + n;
+}
+
+Layout make_layout(int L, int S, const rotor_options &o) {
+    Layout y;
+    y.L = L;
+    y.n = L + 1;
+    y.S = S;
+    y.pitch = ((int64_t)S + 1 + 31) / 32 * 32;  // 256-byte aligned rows
+    y.cells = (int64_t)y.n * (y.n + 1) / 2;
+    y.stack_cap = 4 * y.n + 64;
+    y.ops_cap = max_ops(L);
+    const size_t n2 = (size_t)y.n + 2;
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t r = off;
+        off += al(bytes);
+        return r;
+    };
+    y.off_wx = take(n2 * 4);
+    y.off_wbx = take(n2 * 4);
+    y.off_wy = take(n2 * 4);
+    y.off_of = take(n2 * 4);
+    y.off_ob = take(n2 * 4);
+    y.off_P = take(n2 * 8);
+    y.off_w = take(n2 * 8);
+    y.off_mnull = take((size_t)y.n * y.n * 4);
+    y.off_stack = take((size_t)y.stack_cap * sizeof(int4));
+    y.off_res = take(64);
+    y.off_chain = take(7 * al(n2 * 8));
+    y.off_ops = take((size_t)y.ops_cap * sizeof(rotor_op));
+    y.off_C = take((size_t)y.cells * y.pitch * 8);
+    y.has_D = o.keep_argmin != 0;
+    y.off_D = y.has_D ? take((size_t)y.cells * y.pitch * 2) : 0;
+    y.off_tiled = take(rotor::tiled_extra_bytes(L, S));
+    y.total = off;
+    return y;
+}
+
+rotor::Problem make_problem(const Layout &y, char *ws, const rotor_options &o) {
+    rotor::Problem p{};
+    p.L = y.L;
+    p.n = y.n;
+    p.S = y.S;
+    p.restricted = o.restricted ? 1 : 0;
+    p.pitch = y.pitch;
+    p.wx = (int32_t *)(ws + y.off_wx);
+    p.wbx = (int32_t *)(ws + y.off_wbx);
+    p.wy = (int32_t *)(ws + y.off_wy);
+    p.of = (int32_t *)(ws + y.off_of);
+    p.ob = (int32_t *)(ws + y.off_ob);
+    p.P = (double *)(ws + y.off_P);
+    p.w = (double *)(ws + y.off_w);
+    p.mnullT = (int32_t *)(ws + y.off_mnull);
+    p.stack = (int4 *)(ws + y.off_stack);
+    p.stack_cap = y.stack_cap;
+    p.C = (double *)(ws + y.off_C);
+    p.D = y.has_D ? (uint16_t *)(ws + y.off_D) : nullptr;
+    p.res_cost = (double *)(ws + y.off_res);
+    p.res_nops = (int64_t *)(ws + y.off_res + 8);
+    p.res_status = (int32_t *)(ws + y.off_res + 16);
+    p.ops = (rotor_op *)(ws + y.off_ops);
+    p.ops_cap = y.ops_cap;
+    return p;
+}
+
+rotor_options opts_or_default(const rotor_options *o) {
+    rotor_options r;
+    memset(&r, 0, sizeof r);
+    if (o) r = *o;
+    return r;
+}
+
+int check_args(int32_t L, uint64_t M, int32_t S) {
+    if (L < 1) return fail(ROTOR_EINPUT, "L must be >= 1 (got %d)", L);
+    if (L > 65000) return fail(ROTOR_EINPUT, "L must be <= 65000 (argmin codes are uint16)");
+    if (S < 1) return fail(ROTOR_EINPUT, "slots must be >= 1 (got %d)", S);
+    if (S > (1 << 28)) return fail(ROTOR_EINPUT, "slots too large");
+    if (M == 0) return fail(ROTOR_EINPUT, "mem_limit must be > 0");
+    return ROTOR_OK;
+}
+
+int check_host_chain(const rotor_chain *c, int L) {
+    if (!c || !c->uf || !c->ub || !c->wx || !c->wbx || !c->wy || !c->of || !c->ob)
+        return fail(ROTOR_EINPUT, "chain has a NULL array");
+    for (int i = 0; i <= L; i++) {
+        double a = c->uf[i], b = c->ub[i];
+        if (!(a >= 0.0 && a < INFINITY) || !(b >= 0.0 && b < INFINITY))
+            return fail(ROTOR_EINPUT, "times must be finite and >= 0 (stage %d)", i + 1);
+    }
+    return ROTOR_OK;
+}
+
+// ---- per-thread record of the last solve (export / timings) ----
+struct LastSolve {
+    bool valid = false;
+    Layout y;
+    rotor::Problem p;
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool profiled = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int fill_launches = 0, total_launches = 0;
+};
+thread_local LastSolve g_last;
+
+int ensure_events() {
+    for (auto &e : g_last.ev)
+        if (!e) CK(cudaEventCreate(&e));
+    return ROTOR_OK;
+}
+
+// ---- library-owned cached workspaces (per device) ----
+std::mutex g_cache_mu;
+std::map<int, std::pair<void *, size_t>> g_cache;
+
+int cached_workspace(size_t bytes, void **out) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    auto &e = g_cache[dev];
+    if (e.second < bytes) {
+        if (e.first) {
+            cudaDeviceSynchronize();
+            cudaFree(e.first);
+            e = {nullptr, 0};
+        }
+        void *p = nullptr;
+        cudaError_t err = cudaMalloc(&p, bytes);
+        if (err != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ROTOR_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(err));
+        }
+        e = {p, bytes};
+    }
+    *out = e.first;
+    return ROTOR_OK;
+}
+
+// Enqueue the whole device path for one problem (no host synchronisation).
+// Results go to the workspace's own result/ops areas unless `redirect` is given.
+struct Outputs {
+    double *cost;
+    int64_t *nops;
+    int32_t *status;
+    rotor_op *ops;
+    int64_t ops_cap;
+};
+
+int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws, const rotor_options &o,
+                  cudaStream_t st, const Outputs *redirect) {
+    rotor::Problem p = make_problem(y, ws, o);
+    if (redirect) {
+        p.res_cost = redirect->cost;
+        p.res_nops = redirect->nops;
+        p.res_status = redirect->status;
+        p.ops = redirect->ops;
+        p.ops_cap = redirect->ops_cap;
+    }
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    g_last.valid = true;
+    g_last.y = y;
+    g_last.p = p;
+    g_last.device = dev;
+    g_last.stream = st;
+    g_last.profiled = o.profile != 0;
+    if (o.profile) {
+        int r = ensure_events();
+        if (r) return r;
+        CK(cudaEventRecord(g_last.ev[0], st));
+    }
+    int launches = 0;
+    rotor::launch_precompute(dch, M, p, st);
+    rotor::launch_leaf(p, st);
+    launches += 2;
+    CK(cudaGetLastError());
+    if (o.profile) CK(cudaEventRecord(g_last.ev[1], st));
+    int fill = 0;
+    const bool tiled = (o.kernel == ROTOR_KERNEL_TILED);
+    if (tiled) {
+        fill = rotor::launch_fill_tiled(p, st);
+    } else {
+        for (int d = 1; d <= y.L; d++) rotor::launch_diag_wavefront(p, d, st);
+        fill = y.L;
+    }
+    CK(cudaGetLastError());
+    launches += fill;
+    if (o.profile) CK(cudaEventRecord(g_last.ev[2], st));
+    rotor::launch_reconstruct(p, st);
+    launches += 1;
+    CK(cudaGetLastError());
+    if (o.profile) CK(cudaEventRecord(g_last.ev[3], st));
+    g_last.fill_launches = fill;
+    g_last.total_launches = launches;
+    return ROTOR_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t rotor_version(void) { return 1; }
+
+const char *rotor_last_error(void) { return g_err.c_str(); }
+
+int64_t rotor_max_ops(int32_t L) { return L < 1 ? 0 : max_ops(L); }
+
+double rotor_transitions(int32_t L, int32_t slots) {
+    double n = (double)L + 1, tot = 0;
+    for (int d = 1; d <= L; d++) tot += (n - d) * (d + 1) * ((double)slots + 1);
+    return tot;
+}
+
+int rotor_workspace_bytes(int32_t L, int32_t slots, const rotor_options *opt, uint64_t *bytes) {
+    int r = check_args(L, 1, slots);
+    if (r) return r;
+    if (!bytes) return fail(ROTOR_EINPUT, "bytes is NULL");
+    *bytes = make_layout(L, slots, opts_or_default(opt)).total;
+    return ROTOR_OK;
+}
+
+int rotor_solve_device(const rotor_chain *d_chain, int32_t L, uint64_t mem_limit, int32_t slots,
+                       const rotor_options *opt, void *d_workspace, uint64_t workspace_bytes, void *stream,
+                       double *d_cost, rotor_op *d_ops, int64_t ops_cap, int64_t *d_n_ops, int32_t *d_status) {
+    int r = check_args(L, mem_limit, slots);
+    if (r) return r;
+    if (!d_chain || !d_chain->uf || !d_chain->ub || !d_chain->wx || !d_chain->wbx || !d_chain->wy || !d_chain->of ||
+        !d_chain->ob)
+        return fail(ROTOR_EINPUT, "chain has a NULL array");
+    if (!d_cost || !d_n_ops || !d_status) return fail(ROTOR_EINPUT, "result pointers must be non-NULL");
+    if (ops_cap > 0 && !d_ops) return fail(ROTOR_EINPUT, "d_ops is NULL with ops_cap > 0");
+    const rotor_options o = opts_or_default(opt);
+    Layout y = make_layout(L, slots, o);
+    if (!d_workspace) return fail(ROTOR_EINPUT, "d_workspace is required");
+    if (workspace_bytes < y.total)
+        return fail(ROTOR_ENOMEM, "workspace too small: %llu < %zu", (unsigned long long)workspace_bytes, y.total);
+    Outputs out{d_cost, d_n_ops, d_status, d_ops, ops_cap < 0 ? 0 : ops_cap};
+    return enqueue_solve(*d_chain, mem_limit, y, (char *)d_workspace, o, (cudaStream_t)stream, &out);
+}
+
+int rotor_solve_ex(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int32_t slots, const rotor_options *opt,
+                   void *d_workspace, uint64_t workspace_bytes, void *stream, double *cost_out, rotor_op *ops,
+                   int64_t ops_cap, int64_t *n_ops_out) {
+    int r = check_args(L, mem_limit, slots);
+    if (r) return r;
+    r = check_host_chain(chain, L);
+    if (r) return r;
+    const rotor_options o = opts_or_default(opt);
+    Layout y = make_layout(L, slots, o);
+    void *ws = d_workspace;
+    if (!ws) {
+        r = cached_workspace(y.total, &ws);
+        if (r) return r;
+    } else if (workspace_bytes < y.total) {
+        return fail(ROTOR_ENOMEM, "workspace too small: %llu < %zu", (unsigned long long)workspace_bytes, y.total);
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    char *w = (char *)ws;
+    const size_t n1 = (size_t)L + 1;
+    const size_t seg = al(((size_t)y.n + 2) * 8);
+    char *stage = w + y.off_chain;
+    rotor_chain dch;
+    dch.uf = (const double *)(stage + 0 * seg);
+    dch.ub = (const double *)(stage + 1 * seg);
+    dch.wx = (const uint64_t *)(stage + 2 * seg);
+    dch.wbx = (const uint64_t *)(stage + 3 * seg);
+    dch.wy = (const uint64_t *)(stage + 4 * seg);
+    dch.of = (const uint64_t *)(stage + 5 * seg);
+    dch.ob = (const uint64_t *)(stage + 6 * seg);
+    CK(cudaMemcpyAsync((void *)dch.uf, chain->uf, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.ub, chain->ub, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.wx, chain->wx, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.wbx, chain->wbx, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.wy, chain->wy, (n1 + 1) * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.of, chain->of, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.ob, chain->ob, n1 * 8, cudaMemcpyHostToDevice, st));
+    r = enqueue_solve(dch, mem_limit, y, w, o, st, nullptr);
+    if (r) return r;
+    struct {
+        double cost;
+        int64_t nops;
+        int32_t status;
+    } res;
+    CK(cudaMemcpyAsync(&res.cost, w + y.off_res, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&res.nops, w + y.off_res + 8, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&res.status, w + y.off_res + 16, 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (cost_out) *cost_out = res.cost;
+    if (res.status == ROTOR_INFEASIBLE) {
+        if (n_ops_out) *n_ops_out = 0;
+        if (cost_out) *cost_out = INFINITY;
+        return fail(ROTOR_INFEASIBLE, "infeasible: no persistent schedule within the memory limit");
+    }
+    if (res.status != ROTOR_OK && res.status != ROTOR_ETRUNC)
+        return fail(res.status, "device phase failed with status %d", res.status);
+    if (n_ops_out) *n_ops_out = res.nops;
+    if (ops && ops_cap > 0) {
+        int64_t cnt = std::min<int64_t>(res.nops, ops_cap);
+        if (cnt > 0) {
+            CK(cudaMemcpyAsync(ops, w + y.off_ops, (size_t)cnt * sizeof(rotor_op), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    }
+    if (ops && res.nops > ops_cap) return fail(ROTOR_ETRUNC, "ops truncated: %lld > cap %lld", (long long)res.nops,
+                                               (long long)ops_cap);
+    return ROTOR_OK;
+}
+
+int rotor_solve(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int32_t slots, double *cost_out,
+                rotor_op *ops, int64_t ops_cap, int64_t *n_ops_out) {
+    return rotor_solve_ex(chain, L, mem_limit, slots, nullptr, nullptr, 0, nullptr, cost_out, ops, ops_cap,
+                          n_ops_out);
+}
+
+int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_chains, const uint64_t *limits,
+                      int32_t n_limits, int32_t slots, const rotor_options *opt, void *stream, double *costs,
+                      rotor_op *ops, const int64_t *ops_offsets, const int64_t *ops_caps, int64_t *n_ops,
+                      int32_t *status) {
+    if (!chains || !Ls || !limits || !costs || n_chains < 0 || n_limits < 0)
+        return fail(ROTOR_EINPUT, "bad batch arguments");
+    if (ops && (!ops_offsets || !ops_caps)) return fail(ROTOR_EINPUT, "ops requires ops_offsets and ops_caps");
+    int first_err = ROTOR_OK;
+    for (int i = 0; i < n_chains; i++) {
+        for (int j = 0; j < n_limits; j++) {
+            const int64_t pidx = (int64_t)i * n_limits + j;
+            int64_t cnt = 0;
+            rotor_op *o = ops ? ops + ops_offsets[pidx] : nullptr;
+            int64_t cap = ops ? ops_caps[pidx] : 0;
+            int r = rotor_solve_ex(&chains[i], Ls[i], limits[pidx], slots, opt, nullptr, 0, stream, &costs[pidx], o,
+                                   cap, &cnt);
+            if (status) status[pidx] = r;
+            if (n_ops) n_ops[pidx] = (r == ROTOR_OK || r == ROTOR_ETRUNC) ? cnt : -1;
+            if (r == ROTOR_INFEASIBLE) costs[pidx] = INFINITY;
+            if (r != ROTOR_OK && r != ROTOR_INFEASIBLE && r != ROTOR_ETRUNC && !first_err) first_err = r;
+        }
+    }
+    return first_err;
+}
+
+int rotor_partition_lpt(const double *weights, int32_t n_items, int32_t n_parts, int32_t *part_of) {
+    if (n_items < 0 || n_parts < 1 || (n_items > 0 && (!weights || !part_of)))
+        return fail(ROTOR_EINPUT, "bad partition arguments");
+    std::vector<int> idx(n_items);
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return weights[a] > weights[b]; });
+    std::vector<double> load(n_parts, 0.0);
+    for (int i : idx) {
+        int best = 0;
+        for (int q = 1; q < n_parts; q++)
+            if (load[q] < load[best]) best = q;
+        part_of[i] = best;
+        load[best] += weights[i];
+    }
+    return ROTOR_OK;
+}
+
+int rotor_export_tables(double *C_host, uint16_t *D_host, int64_t n_values) {
+    if (!g_last.valid) return fail(ROTOR_EINPUT, "no solve on this thread");
+    const Layout &y = g_last.y;
+    const int64_t want = y.cells * (y.S + 1);
+    if (n_values != want) return fail(ROTOR_EINPUT, "n_values %lld != %lld", (long long)n_values, (long long)want);
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev != g_last.device) CK(cudaSetDevice(g_last.device));
+    CK(cudaStreamSynchronize(g_last.stream));
+    const size_t row = (size_t)(y.S + 1);
+    if (C_host)
+        CK(cudaMemcpy2D(C_host, row * 8, g_last.p.C, (size_t)y.pitch * 8, row * 8, (size_t)y.cells,
+                        cudaMemcpyDeviceToHost));
+    if (D_host) {
+        if (g_last.p.D) {
+            CK(cudaMemcpy2D(D_host, row * 2, g_last.p.D, (size_t)y.pitch * 2, row * 2, (size_t)y.cells,
+                            cudaMemcpyDeviceToHost));
+        } else {
+            uint16_t *tmp = nullptr;
+            CK(cudaMalloc(&tmp, (size_t)y.cells * row * 2));
+            for (int d = 0; d <= y.L; d++) rotor::launch_derive_argmin(g_last.p, d, tmp, (int64_t)row, 0);
+            cudaError_t e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaDeviceSynchronize();
+            if (e == cudaSuccess) e = cudaMemcpy(D_host, tmp, (size_t)y.cells * row * 2, cudaMemcpyDeviceToHost);
+            cudaFree(tmp);
+            if (e != cudaSuccess) return fail(ROTOR_EDEVICE, "derive argmin: %s", cudaGetErrorString(e));
+        }
+    }
+    if (dev != g_last.device) CK(cudaSetDevice(dev));
+    return ROTOR_OK;
+}
+
+int rotor_export_rows(const int32_t *s, const int32_t *t, int64_t n_rows, double *C_host) {
+    if (!g_last.valid) return fail(ROTOR_EINPUT, "no solve on this thread");
+    if (n_rows < 0 || (n_rows > 0 && (!s || !t || !C_host))) return fail(ROTOR_EINPUT, "bad export_rows arguments");
+    const Layout &y = g_last.y;
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev != g_last.device) CK(cudaSetDevice(g_last.device));
+    CK(cudaStreamSynchronize(g_last.stream));
+    const size_t row = (size_t)(y.S + 1);
+    for (int64_t r = 0; r < n_rows; r++) {
+        if (s[r] < 1 || t[r] < s[r] || t[r] > y.n) return fail(ROTOR_EINPUT, "bad cell (%d,%d)", s[r], t[r]);
+        const double *src = g_last.p.C + rotor::cell_index(y.n, s[r], t[r]) * y.pitch;
+        CK(cudaMemcpy(C_host + r * row, src, row * 8, cudaMemcpyDeviceToHost));
+    }
+    if (dev != g_last.device) CK(cudaSetDevice(dev));
+    return ROTOR_OK;
+}
+
+int rotor_last_timings(rotor_timings *out) {
+    if (!out) return fail(ROTOR_EINPUT, "out is NULL");
+    if (!g_last.valid || !g_last.profiled) return fail(ROTOR_EINPUT, "last solve was not profiled");
+    CK(cudaEventSynchronize(g_last.ev[3]));
+    float a = 0, b = 0, c = 0;
+    CK(cudaEventElapsedTime(&a, g_last.ev[0], g_last.ev[1]));
+    CK(cudaEventElapsedTime(&b, g_last.ev[1], g_last.ev[2]));
+    CK(cudaEventElapsedTime(&c, g_last.ev[2], g_last.ev[3]));
+    out->pre_ms = a;
+    out->fill_ms = b;
+    out->reconstruct_ms = c;
+    out->fill_launches = g_last.fill_launches;
+    out->total_launches = g_last.total_launches;
+    return ROTOR_OK;
+}
+
+int rotor_release(void) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    int dev0 = 0;
+    cudaGetDevice(&dev0);
+    for (auto &kv : g_cache) {
+        if (kv.second.first) {
+            cudaSetDevice(kv.first);
+            cudaDeviceSynchronize();
+            cudaFree(kv.second.first);
+        }
+    }
+    g_cache.clear();
+    cudaSetDevice(dev0);
+    g_last.valid = false;
+    return ROTOR_OK;
+}
+
+}  // extern "C"

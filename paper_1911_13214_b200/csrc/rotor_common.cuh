@@ -1,0 +1,58 @@
+// Shared device-side definitions of the B200 solver (product path only; the
+// oracle in oracle/ never includes this file).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rotor.h"
+
+namespace rotor {
+
+constexpr uint16_t kNone = 0xFFFF;  // D code of an infeasible cell
+constexpr int kStatusOk = ROTOR_OK;
+
+// Device view of one DP problem inside a workspace.
+//
+// Indices follow the paper (1-based stages, n = L+1):
+//   wx[l] l=0..L, wy[l] l=0..n, wbx/of/ob[l] l=1..n   (int32 slots, clamped to S+1)
+//   P[k] = uf[1] + ... + uf[k] (sequential fp64), k = 0..n
+//   w[s] = uf[s] + ub[s]
+//   mnullT[(t-1)*n + (s-1)] = m_null(s,t), s < t
+// Table C: cell(s,t) = d*n - d*(d-1)/2 + (s-1), d = t-s (d-major, the canonical
+// layout of include/rotor.h); row of a cell = pitch doubles, m = 0..S.
+struct Problem {
+    int L, n, S;
+    int restricted;
+    int64_t pitch;  // doubles per cell row
+    int32_t *wx, *wbx, *wy, *of, *ob;
+    double *P, *w;
+    int32_t *mnullT;
+    double *C;
+    uint16_t *D;  // nullable
+    // reconstruction / results
+    int4 *stack;
+    int32_t stack_cap;
+    double *res_cost;
+    int64_t *res_nops;
+    int32_t *res_status;
+    rotor_op *ops;
+    int64_t ops_cap;
+};
+
+__host__ __device__ inline int64_t cell_index(int n, int s, int t) {
+    int64_t d = t - s;
+    return d * n - d * (d - 1) / 2 + (s - 1);
+}
+
+__device__ __forceinline__ int m_all(const Problem &p, int s, int t) {
+    // m_all(s,t) = max(wy[t] + wbx[s] + of[s], wy[s] + wbx[s] + ob[s])
+    int a = p.wy[t] + p.wbx[s] + p.of[s];
+    int b = p.wy[s] + p.wbx[s] + p.ob[s];
+    return a > b ? a : b;
+}
+
+__device__ __forceinline__ int m_null(const Problem &p, int s, int t) {
+    return p.mnullT[(int64_t)(t - 1) * p.n + (s - 1)];
+}
+
+}  // namespace rotor

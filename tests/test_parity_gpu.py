@@ -1,0 +1,232 @@
+"""GPU parity: the CUDA path (through the C ABI) against the independent oracle.
+
+Bar (north_star): bit-exact fp64 C tables (compared as uint64
+bit patterns, tolerance 0 ulp), identical argmin tables D (uint16), identical
+costs and identical Algorithm-2 schedules; replaying the GPU schedule in the
+oracle's simulator is valid within the limit and reproduces the cost.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import chaingen as G
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def R():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import __graft_entry__ as ge
+
+    ge.build_library()
+    import paper_1911_13214_b200 as R
+
+    return R
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def assert_tables_equal(Cg, Co, what=""):
+    if not np.array_equal(bits(Cg), bits(Co)):
+        bad = np.argwhere(bits(Cg) != bits(Co))
+        i, m = bad[0]
+        raise AssertionError(f"{what}: {len(bad)} cells differ; first cell {i} m={m}: gpu={Cg[i, m]!r} oracle={Co[i, m]!r}")
+
+
+KERNELS = ["wavefront", "tiled"]
+
+
+def gpu_full(R, ch, M, S, **opts):
+    res = R.solve(ch, M, S, **opts)
+    C, D = R.export_tables(ch.L + 1, S)
+    return res, C, D
+
+
+def check_against_oracle(R, O, ch, M, S, restricted=False, kernel="wavefront", keep_argmin=False):
+    o = O.OracleSolve(ch, M, S, restricted=restricted)
+    Co, Do = o.tables()
+    res, Cg, Dg = gpu_full(R, ch, M, S, restricted=restricted, kernel=kernel, keep_argmin=keep_argmin)
+    assert_tables_equal(Cg, Co, f"{ch.name} M={M} S={S} {kernel}")
+    assert np.array_equal(Dg, Do), f"argmin tables differ ({kernel}, keep_argmin={keep_argmin})"
+    oc = o.cost
+    if math.isinf(oc):
+        assert res.status == R.INFEASIBLE and math.isinf(res.cost)
+    else:
+        assert res.status == R.OK
+        assert bits(np.array([res.cost])) == bits(np.array([oc]))
+        ops_o = o.reconstruct()
+        assert res.op_list() == ops_o
+        sz = o.sizes()
+        rep = O.simulate(res.op_list(), sz, S)
+        assert rep.valid, rep.failure
+        assert abs(rep.makespan - oc) <= len(ops_o) * math.ulp(oc)
+    return o, res
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_tiny_random_chains(R, oracle_mod, kernel):
+    """Random small chains: ties (integer/zero times), zero sizes, huge abar/a,
+    general (independent delta, abar < a) chains, L = 1, infeasible limits."""
+    O = oracle_mod
+    rng = G.SplitMix64(17)
+    for it in range(60):
+        L = 1 + rng.randint(0, 24)
+        kind = it % 4
+        if kind == 0:
+            ch = G.tiny_chain(rng, L, size_max=5, time_max=3, allow_zero_time=True)
+        elif kind == 1:
+            ch = G.tiny_chain(rng, L, size_max=6, abar_ge_a=False, delta_eq_a=False)
+        elif kind == 2:
+            ch = G.tiny_chain(rng, L, size_max=4, int_times=False)
+        else:
+            ch = G.random_chain(rng, L, real_times=bool(it % 8 == 3), big=True)
+        S = [7, 16, 33, 64, 130][rng.randint(0, 4)]
+        if kind == 3:
+            M = max(1, int(sum(int(x) for x in ch.wbx) * (0.05 + 0.5 * rng.uniform())))
+        else:
+            M = S
+        check_against_oracle(R, O, ch, M, S, kernel=kernel, keep_argmin=(it % 5 == 0 and kernel == "wavefront"))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_restricted_mode(R, oracle_mod, kernel):
+    O = oracle_mod
+    rng = G.SplitMix64(23)
+    for it in range(10):
+        ch = G.tiny_chain(rng, 3 + rng.randint(0, 20), size_max=4)
+        check_against_oracle(R, O, ch, 40, 40, restricted=True, kernel=kernel)
+    check_against_oracle(R, O, G.unit_chain(40, ub=0.0), 14, 14, restricted=True, kernel=kernel)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config1_and_2_full_tables(R, oracle_mod, kernel):
+    O = oracle_mod
+    for p in (G.config1(), G.config2()):
+        check_against_oracle(R, O, p.chain, p.mem_limit, p.slots, kernel=kernel)
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_edge_cases(R, oracle_mod, kernel):
+    O = oracle_mod
+    # L = 1, ample memory -> [F_all1, F_all2, B2, B1]
+    o, res = check_against_oracle(R, O, G.unit_chain(1), 100, 100, kernel=kernel)
+    assert res.op_list() == [(0, 1), (0, 2), (3, 2), (3, 1)]
+    # infeasible: a^0 alone exceeds M (m_top < 0)
+    ch = G.unit_chain(3, size=10)
+    res = R.solve(ch, 5, 5, kernel=kernel)
+    assert res.status == R.INFEASIBLE and math.isinf(res.cost)
+    # infeasible: m_top >= 0 but too small
+    res = R.solve(G.unit_chain(5), 3, 3, kernel=kernel)
+    assert res.status == R.INFEASIBLE
+    # all sizes zero, S = 1: store-all at zero memory
+    z = G.Chain(L=4, uf=[1, 2, 3, 4, 5], ub=[1] * 5, wx=[0] * 5, wbx=[0] * 5, wy=[0] * 6, of=[0] * 5, ob=[0] * 5)
+    check_against_oracle(R, O, z, 1, 1, kernel=kernel)
+    # one huge item (clamped slot count > S) must behave like the oracle's uncapped count
+    ch = G.unit_chain(6)
+    ch.wbx[3] = 10**15
+    check_against_oracle(R, O, ch, 20, 20, kernel=kernel)
+    # ops truncation reports ETRUNC with the full count
+    p = G.config1()
+    full = R.solve(p.chain, p.mem_limit, 12, kernel=kernel)
+    tr = R.solve(p.chain, p.mem_limit, 12, ops_cap=5, kernel=kernel)
+    assert tr.status == R.ETRUNC and tr.n_ops == full.n_ops and tr.op_list() == full.op_list()[:5]
+
+
+def test_device_resident_path(R, oracle_mod):
+    import torch
+
+    O = oracle_mod
+    p = G.config2()
+    ch = p.chain
+    dev = torch.device("cuda:0")
+    d = {k: torch.from_numpy(np.asarray(getattr(ch, k)).astype(np.float64 if k in ("uf", "ub") else np.int64)).to(dev)
+         for k in ("uf", "ub", "wx", "wbx", "wy", "of", "ob")}
+    ws = torch.empty(R.workspace_bytes(ch.L, p.slots), dtype=torch.uint8, device=dev)
+    cap = R.max_ops(ch.L)
+    out = dict(cost=torch.empty(1, dtype=torch.float64, device=dev), ops=torch.empty((cap, 2), dtype=torch.int32, device=dev),
+               n_ops=torch.empty(1, dtype=torch.int64, device=dev), status=torch.empty(1, dtype=torch.int32, device=dev))
+    st = torch.cuda.current_stream()
+    R.solve_device(d, ch.L, p.mem_limit, p.slots, ws, out, stream=st)
+    torch.cuda.synchronize()
+    o = O.OracleSolve(ch, p.mem_limit, p.slots)
+    assert int(out["status"].item()) == R.OK
+    assert out["cost"].item() == o.cost
+    k = int(out["n_ops"].item())
+    ops = [tuple(map(int, r)) for r in out["ops"][:k].cpu().numpy()]
+    assert ops == o.reconstruct()
+    C, _ = R.export_tables(ch.L + 1, p.slots, D=False)
+    assert_tables_equal(C, o.tables()[0], "device path")
+
+
+def test_batched_equals_single(R, oracle_mod):
+    O = oracle_mod
+    chains, limits, S = G.config5(n_limits=6)
+    chains, limits = chains[:4], limits[:4]
+    costs, status, n_ops, ops = R.solve_batch(chains, limits, S, with_ops=True)
+    for i, ch in enumerate(chains):
+        for j, M in enumerate(limits[i]):
+            o = O.OracleSolve(ch, M, S)
+            c = o.cost
+            if math.isinf(c):
+                assert status[i, j] == R.INFEASIBLE and math.isinf(costs[i, j])
+            else:
+                assert status[i, j] == R.OK
+                assert costs[i, j] == c
+                got = [tuple(map(int, r)) for r in ops[i * len(limits[i]) + j]]
+                assert got == o.reconstruct()
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config3_full_table(R, oracle_mod, kernel):
+    """DenseNet-shaped chain, L=300, S=2000 (9.2e9 transitions): full-table bit parity."""
+    O = oracle_mod
+    p = G.config3()
+    check_against_oracle(R, O, p.chain, p.mem_limit, p.slots, kernel=kernel)
+
+
+def _window_cells(s0, t0):
+    return [(s, t) for d in range(0, t0 - s0 + 1) for s in range(s0, t0 - d + 1) for t in [s + d]]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config4_full_size_sampled(R, oracle_mod, kernel):
+    """L=1000, S=4000 in the bench's launch configuration: every cell of several
+    windows of stages (start, middle, end with the loss stage, one long window)
+    is bit-identical to the oracle's windowed fill; the top schedule replays
+    valid within S slots with the reported cost; rows are monotone in m."""
+    O = oracle_mod
+    p = G.config4()
+    ch = p.chain
+    res = R.solve(ch, p.mem_limit, p.slots, kernel=kernel)
+    assert res.status == R.OK
+    n = ch.L + 1
+    for (s0, t0) in [(1, 40), (480, 530), (950, n), (300, 420)]:
+        o = O.OracleSolve(ch, p.mem_limit, p.slots, window=(s0, t0))
+        Co, _ = o.tables()
+        cells = _window_cells(s0, t0)
+        Cg = R.export_rows(cells, p.slots)
+        nw = t0 - s0 + 1
+        Co_rows = np.stack([Co[O.cell_index(nw, s - s0 + 1, t - s0 + 1)] for s, t in cells])
+        assert_tables_equal(Cg, Co_rows, f"cfg4 window {s0}..{t0}")
+        assert np.all(Cg[:, 1:] <= Cg[:, :-1])
+    # top cell: schedule replay in the oracle simulator (the oracle cannot fill L=1000 in a test)
+    o = O.OracleSolve(ch, p.mem_limit, p.slots, fill=False)
+    sz = o.sizes()
+    rep = O.simulate(res.op_list(), sz, p.slots)
+    assert rep.valid, rep.failure
+    assert abs(rep.makespan - res.cost) <= res.n_ops * math.ulp(res.cost)
+    lb = float(np.sum(ch.uf) + np.sum(ch.ub))
+    assert res.cost >= lb * (1 - 1e-12)
+    top = R.export_rows([(1, n)], p.slots)[0]
+    assert top[S_top(sz, p.slots)] == res.cost
+
+
+def S_top(sz, S):
+    return S - sz.wx[0]
