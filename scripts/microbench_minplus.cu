@@ -1,0 +1,91 @@
+// Microbenchmark: sustained min-plus transition rate of the B200 SM for the
+// inner loop shape of the tiled fill (register tile RS x RT, operands from
+// shared memory, m along lanes).  Three min variants:
+//   0: v < acc ? v : acc on doubles       (DADD + DSETP + 2 FSEL)
+//   1: 64-bit integer min on the bit patterns of non-negative doubles
+//   2: DADD only (upper bound of the fp64 pipe)
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb microbench_minplus.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+template <int MODE, int RS, int RT>
+__global__ void __launch_bounds__(256) kern(double *out, int iters) {
+    __shared__ double As[8][RS][32];
+    __shared__ double Bs[8][RT][32];
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 8 * RS * 32; i += blockDim.x) (&As[0][0][0])[i] = 1.0 + (i % 7) * 0.125;
+    for (int i = threadIdx.x; i < 8 * RT * 32; i += blockDim.x) (&Bs[0][0][0])[i] = 2.0 + (i % 5) * 0.25;
+    __syncthreads();
+    double acc[RS][RT];
+#pragma unroll
+    for (int i = 0; i < RS; i++)
+#pragma unroll
+        for (int j = 0; j < RT; j++) acc[i][j] = 1e300;
+    for (int it = 0; it < iters; it++) {
+#pragma unroll 4
+        for (int k = 0; k < 8; k++) {
+            double a[RS], b[RT];
+#pragma unroll
+            for (int i = 0; i < RS; i++) a[i] = As[k][i][lane];
+#pragma unroll
+            for (int j = 0; j < RT; j++) b[j] = Bs[k][j][lane];
+#pragma unroll
+            for (int i = 0; i < RS; i++)
+#pragma unroll
+                for (int j = 0; j < RT; j++) {
+                    double v = __dadd_rn(a[i], b[j]);
+                    if (MODE == 0) {
+                        acc[i][j] = v < acc[i][j] ? v : acc[i][j];
+                    } else if (MODE == 1) {
+                        long long x = __double_as_longlong(v), y = __double_as_longlong(acc[i][j]);
+                        acc[i][j] = __longlong_as_double(x < y ? x : y);
+                    } else {
+                        acc[i][j] = __dadd_rn(acc[i][j], v) ;
+                    }
+                }
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int i = 0; i < RS; i++)
+#pragma unroll
+        for (int j = 0; j < RT; j++) s += acc[i][j];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
+template <int MODE, int RS, int RT>
+void run(const char *name) {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = sms * 2, threads = 256, iters = 3200;
+    double *out;
+    cudaMalloc(&out, blocks * threads * sizeof(double));
+    kern<MODE, RS, RT><<<blocks, threads>>>(out, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    kern<MODE, RS, RT><<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double tr = (double)blocks * threads * iters * 8 * RS * RT;
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("%-28s RS=%d RT=%d  %.3e transitions/s  (%.1f tr/clk/SM at %d MHz)  err=%s\n", name, RS, RT, tr / (ms * 1e-3),
+           tr / (ms * 1e-3) / sms / (clk * 1e3), clk / 1000, cudaGetErrorString(cudaGetLastError()));
+    cudaFree(out);
+}
+
+int main() {
+    run<0, 4, 4>("dsetp-min");
+    run<0, 4, 8>("dsetp-min");
+    run<0, 8, 8>("dsetp-min");
+    run<1, 4, 8>("int64-min");
+    run<1, 8, 8>("int64-min");
+    run<2, 4, 8>("dadd-only");
+    run<2, 8, 8>("dadd-only");
+    return 0;
+}
