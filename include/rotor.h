@@ -159,7 +159,7 @@ double rotor_transitions(int32_t L, int32_t slots);
  * Parity / debug: copy the tables of the LAST solve made by this thread
  * (rotor_solve / rotor_solve_ex / rotor_solve_device) to host memory, in the
  * canonical layout
- *     cell(s,t) = d*n - d*(d-1)/2 + (s-1),  d = t-s, n = L+1
+ *     cell(s,t) = (s-1)*n - (s-1)*(s-2)/2 + (t-s), n = L+1   (s-major)
  *     C_host[cell*(S+1) + m], m = 0..S      (fp64; +inf = infeasible)
  *     D_host[cell*(S+1) + m]                (uint16: k = s'-s for an F_ck split,
  *                                            0 for F_all / leaf, 0xFFFF if C = +inf)

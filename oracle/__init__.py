@@ -101,9 +101,9 @@ def slots_of(x: int, M: int, S: int) -> int:
 
 
 def cell_index(n: int, s: int, t: int) -> int:
-    """Canonical table layout (include/rotor.h): d-major, then s."""
-    d = t - s
-    return d * n - d * (d - 1) // 2 + (s - 1)
+    """Canonical table layout (include/rotor.h): s-major, then t."""
+    r = s - 1  # s-major: row r holds cells (s, s..n)
+    return r * n - r * (r - 1) // 2 + (t - s)
 
 
 @dataclass

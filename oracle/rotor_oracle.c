@@ -20,7 +20,7 @@
  *   wy[l]                                 l = 0..n   (delta^l)
  * Memory index m = 0..S (Q6).  +inf is IEEE +INFINITY (Q13).
  * Exported table layout ("canonical", documented in include/rotor.h):
- *   cell(s,t) = d*n - d*(d-1)/2 + (s-1),  d = t-s;  value at cell*(S+1) + m.
+ *   cell(s,t) = (s-1)*n - (s-1)*(s-2)/2 + (t-s)  (s-major);  value at cell*(S+1) + m.
  * D (argmin) codes: k = s'-s in 1..d for an F_ck split, 0 for F_all / leaf,
  *   0xFFFF when C = +inf.
  *
@@ -72,8 +72,8 @@ static int64_t slots_of(uint64_t x, uint64_t M, int S)
 
 static int64_t cell_index(const oracle_ctx *c, int s, int t)
 {
-    int64_t d = t - s;
-    return d * c->nw - d * (d - 1) / 2 + (s - c->s0);
+    int64_t r = s - c->s0; /* s-major: row r holds cells (s, s..s0+nw-1) */
+    return r * c->nw - r * (r - 1) / 2 + (t - s);
 }
 
 static double *Cp(oracle_ctx *c, int s, int t) { return c->C + cell_index(c, s, t) * (int64_t)(c->S + 1); }

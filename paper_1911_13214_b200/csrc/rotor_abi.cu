@@ -46,10 +46,19 @@ struct Layout {
     int stack_cap = 0;
     int64_t ops_cap = 0;
     size_t off_wx, off_wbx, off_wy, off_of, off_ob, off_P, off_w, off_mnull, off_stack, off_res;
-    size_t off_chain, off_ops, off_C, off_D, off_tiled;
+    size_t off_chain, off_ops, off_C, off_D, off_A, off_tiled;
     size_t total = 0;
     bool has_D = false;
+    bool has_A = false;
 };
+
+// The tiled fill is the default (AUTO); the wavefront kernel is used when
+// requested explicitly or when the argmin table D is recorded during the fill.
+bool uses_tiled(const rotor_options &o) {
+    if (o.kernel == ROTOR_KERNEL_TILED) return true;
+    if (o.kernel == ROTOR_KERNEL_WAVEFRONT) return false;
+    return o.keep_argmin == 0;
+}
 
 int64_t max_ops(int L) {
     int64_t n = (int64_t)L + 1;
@@ -87,6 +96,8 @@ Layout make_layout(int L, int S, const rotor_options &o) {
     y.off_C = take((size_t)y.cells * y.pitch * 8);
     y.has_D = o.keep_argmin != 0;
     y.off_D = y.has_D ? take((size_t)y.cells * y.pitch * 2) : 0;
+    y.has_A = uses_tiled(o);
+    y.off_A = y.has_A ? take((size_t)y.cells * y.pitch * 8) : 0;
     y.off_tiled = take(rotor::tiled_extra_bytes(L, S));
     y.total = off;
     return y;
@@ -111,6 +122,7 @@ rotor::Problem make_problem(const Layout &y, char *ws, const rotor_options &o) {
     p.stack_cap = y.stack_cap;
     p.C = (double *)(ws + y.off_C);
     p.D = y.has_D ? (uint16_t *)(ws + y.off_D) : nullptr;
+    p.A = y.has_A ? (double *)(ws + y.off_A) : nullptr;
     p.res_cost = (double *)(ws + y.off_res);
     p.res_nops = (int64_t *)(ws + y.off_res + 8);
     p.res_status = (int32_t *)(ws + y.off_res + 16);
@@ -232,9 +244,12 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
     CK(cudaGetLastError());
     if (o.profile) CK(cudaEventRecord(g_last.ev[1], st));
     int fill = 0;
-    const bool tiled = (o.kernel == ROTOR_KERNEL_TILED);
-    if (tiled) {
+    if (y.has_A) {
         fill = rotor::launch_fill_tiled(p, st);
+        if (fill < 0) {
+            cudaError_t e = cudaGetLastError();
+            return fail(ROTOR_EDEVICE, "tiled fill launch failed: %s", cudaGetErrorString(e));
+        }
     } else {
         for (int d = 1; d <= y.L; d++) rotor::launch_diag_wavefront(p, d, st);
         fill = y.L;

@@ -18,7 +18,7 @@ constexpr int kStatusOk = ROTOR_OK;
 //   P[k] = uf[1] + ... + uf[k] (sequential fp64), k = 0..n
 //   w[s] = uf[s] + ub[s]
 //   mnullT[(t-1)*n + (s-1)] = m_null(s,t), s < t
-// Table C: cell(s,t) = d*n - d*(d-1)/2 + (s-1), d = t-s (d-major, the canonical
+// Table C: cell(s,t) = (s-1)*n - (s-1)*(s-2)/2 + (t-s) (s-major, the canonical
 // layout of include/rotor.h); row of a cell = pitch doubles, m = 0..S.
 struct Problem {
     int L, n, S;
@@ -29,6 +29,7 @@ struct Problem {
     int32_t *mnullT;
     double *C;
     uint16_t *D;  // nullable
+    double *A;    // nullable: A(s,c,m) = fl(fl(P[c]-P[s-1]) + C(s,c,m)), same layout as C (tiled fill)
     // reconstruction / results
     int4 *stack;
     int32_t stack_cap;
@@ -40,8 +41,8 @@ struct Problem {
 };
 
 __host__ __device__ inline int64_t cell_index(int n, int s, int t) {
-    int64_t d = t - s;
-    return d * n - d * (d - 1) / 2 + (s - 1);
+    int64_t r = s - 1;  // s-major: cells (s, s..n) are contiguous rows
+    return r * n - r * (r - 1) / 2 + (t - s);
 }
 
 __device__ __forceinline__ int m_all(const Problem &p, int s, int t) {

@@ -73,8 +73,10 @@ __global__ void k_leaf(Problem p) {
     if (m > p.S) return;
     const int ma = m_all(p, s, s);
     const int64_t off = cell_index(p.n, s, s) * p.pitch + m;
-    p.C[off] = (m >= ma) ? p.w[s] : INFINITY;
+    const double c = (m >= ma) ? p.w[s] : INFINITY;
+    p.C[off] = c;
     if (p.D) p.D[off] = (m >= ma) ? 0 : kNone;
+    if (p.A && s < p.n) p.A[off] = __dadd_rn(__dadd_rn(p.P[s], -p.P[s - 1]), c);
 }
 
 // ---------------------------------------------------------------------------
