@@ -320,16 +320,27 @@ def run_ours(args):
     value = world * tr * args.steps / (elapsed_ms / 1e3)
     peaks, peak_kind = measured_peaks()
     fill_avg_ms = sum(fill_ms) / len(fill_ms)
-    use_tiled = kernel == "tiled"
-    if use_tiled:
-        roof = None  # filled by the tiled model below
-    b_alg = alg_bytes_wavefront(L, S)
-    achieved = b_alg / (fill_avg_ms / 1e3) / 1e9  # GB/s, fill phase = all K2 launches
-    peak = float(peaks["hbm_gbs"])
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": ncu_traffic("k_diag_wavefront"), "kernel": "k_diag_wavefront (all diagonals d=1..L)",
-                "alg_bytes_per_step": b_alg, "launches_per_step": fill_launches, "peak_source": peak_kind,
-                "fill_ms_per_step": fill_avg_ms}
+    if kernel in ("auto", "tiled"):
+        # Tiled fill: bound by the fp64 pipe: every transition is one
+        # DADD + one DSETP (+2 FSEL on the ALU pipe); B200 issues 64 fp64 lanes/clk/SM.
+        clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
+        peak = 148 * 64 * clk_mhz * 1e6 / 2 / 1e9  # Gtransitions/s
+        achieved = tr / (fill_avg_ms / 1e3) / 1e9
+        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gtransitions/s",
+                    "frac": achieved / peak, "traffic": ncu_traffic("k_tile_middle"),
+                    "kernel": "tiled fill (k_tile_middle + k_tile_dep, all tile diagonals)",
+                    "peak_model": "148 SMs x 64 fp64 lanes/clk x sm_max_mhz / 2 fp64 ops per transition",
+                    "launches_per_step": fill_launches, "fill_ms_per_step": fill_avg_ms,
+                    "hbm_wavefront_equiv_frac": alg_bytes_wavefront(L, S) / (fill_avg_ms / 1e3) / 1e9
+                    / float(peaks["hbm_gbs"])}
+    else:
+        b_alg = alg_bytes_wavefront(L, S)
+        achieved = b_alg / (fill_avg_ms / 1e3) / 1e9  # GB/s, fill phase = all K2 launches
+        peak = float(peaks["hbm_gbs"])
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": ncu_traffic("k_diag_wavefront"), "kernel": "k_diag_wavefront (all diagonals d=1..L)",
+                    "alg_bytes_per_step": b_alg, "launches_per_step": fill_launches, "peak_source": peak_kind,
+                    "fill_ms_per_step": fill_avg_ms}
 
     cpu = None
     if not args.no_cpu_baseline:
