@@ -70,7 +70,7 @@ Layout make_layout(int L, int S, const rotor_options &o) {
     y.L = L;
     y.n = L + 1;
     y.S = S;
-    y.pitch = ((int64_t)S + 1 + 31) / 32 * 32;  // 256-byte aligned rows
+    y.pitch = ((int64_t)rotor::kPad + S + 1 + 31) / 32 * 32;  // 256-byte aligned rows, left pad
     y.cells = (int64_t)y.n * (y.n + 1) / 2;
     y.stack_cap = 4 * y.n + 64;
     y.ops_cap = max_ops(L);
@@ -93,11 +93,11 @@ Layout make_layout(int L, int S, const rotor_options &o) {
     y.off_res = take(64);
     y.off_chain = take(7 * al(n2 * 8));
     y.off_ops = take((size_t)y.ops_cap * sizeof(rotor_op));
-    y.off_C = take((size_t)y.cells * y.pitch * 8);
+    y.off_C = take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 8);
     y.has_D = o.keep_argmin != 0;
     y.off_D = y.has_D ? take((size_t)y.cells * y.pitch * 2) : 0;
     y.has_A = uses_tiled(o);
-    y.off_A = y.has_A ? take((size_t)y.cells * y.pitch * 8) : 0;
+    y.off_A = y.has_A ? take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 8) : 0;
     y.off_tiled = take(rotor::tiled_extra_bytes(L, S));
     y.total = off;
     return y;
@@ -120,9 +120,9 @@ rotor::Problem make_problem(const Layout &y, char *ws, const rotor_options &o) {
     p.mnullT = (int32_t *)(ws + y.off_mnull);
     p.stack = (int4 *)(ws + y.off_stack);
     p.stack_cap = y.stack_cap;
-    p.C = (double *)(ws + y.off_C);
-    p.D = y.has_D ? (uint16_t *)(ws + y.off_D) : nullptr;
-    p.A = y.has_A ? (double *)(ws + y.off_A) : nullptr;
+    p.C = (double *)(ws + y.off_C) + rotor::kPad;  // column m = 0 of row 0
+    p.D = y.has_D ? (uint16_t *)(ws + y.off_D) + rotor::kPad : nullptr;
+    p.A = y.has_A ? (double *)(ws + y.off_A) + rotor::kPad : nullptr;
     p.res_cost = (double *)(ws + y.off_res);
     p.res_nops = (int64_t *)(ws + y.off_res + 8);
     p.res_status = (int32_t *)(ws + y.off_res + 16);

@@ -9,6 +9,12 @@
 namespace rotor {
 
 constexpr uint16_t kNone = 0xFFFF;  // D code of an infeasible cell
+// Table rows carry kPad columns left of m = 0 and the tables kPadRows spare
+// rows at the end, so every TMA box of the tiled fill (m0 - shift >= -kPad,
+// row + box height <= rows + kPadRows) lies inside the allocation.  The pads
+// only ever feed candidates of cells the m_null gate discards (DESIGN Q6).
+constexpr int kPad = 16;
+constexpr int kPadRows = 32;
 constexpr int kStatusOk = ROTOR_OK;
 
 // Device view of one DP problem inside a workspace.

@@ -103,12 +103,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         double *a_dst = As + st * A_STAGE;
         for (int a = 0; a < TB; a++) {
             const int s = i0 + a;  // cells (s, sp0-1 .. sp0+KC-2)
-            tma_load_2d(a_dst + a * KC * TM, &tmA, m0, (int)cell_index(n, s, sp0 - 1), bar);
+            tma_load_2d(a_dst + a * KC * TM, &tmA, m0 + kPad, (int)cell_index(n, s, sp0 - 1), bar);
         }
         double *b_dst = Bs + st * B_STAGE;
         for (int k = 0; k < KC; k++) {
             const int sp = sp0 + k;  // cells (sp, j0 .. j0+TB-1) at m - wx[sp-1]
-            tma_load_2d(b_dst + k * TB * TM, &tmC, m0 - p.wx[sp - 1], (int)cell_index(n, sp, j0), bar);
+            // A chunk whose shifted window starts below -kPad lies wholly under
+            // m = wx[sp-1] <= m_null(s,t): every cell it feeds is gated, so the
+            // (clamped) values loaded for it are never used (DESIGN Q6).
+            const int c0 = max(m0 - p.wx[sp - 1], -kPad) + kPad;
+            tma_load_2d(b_dst + k * TB * TM, &tmC, c0, (int)cell_index(n, sp, j0), bar);
         }
     };
 
@@ -300,8 +304,10 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
     const int n = p.n;
     const int nb = (n + TB - 1) / TB;
     const int64_t rows = (int64_t)n * (n + 1) / 2;
-    CUtensorMap tmA, tmC;
-    if (!make_map(&tmA, p.A, rows, p.pitch, KC) || !make_map(&tmC, p.C, rows, p.pitch, TB)) return -1;
+    CUtensorMap tmA, tmC;  // over the whole allocations: left pad columns and spare rows included
+    if (!make_map(&tmA, p.A - kPad, rows + kPadRows, p.pitch, KC) ||
+        !make_map(&tmC, p.C - kPad, rows + kPadRows, p.pitch, TB))
+        return -1;
     const int dep_blocks = dep_grid_blocks();
     int launches = 0;
     for (int delta = 0; delta < nb; delta++) {
