@@ -118,7 +118,10 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) mbar_init(&bars[s], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // make the initialised barriers visible to the async (TMA) proxy; the
+        // .cluster-scoped fence.mbarrier_init faults in a non-cluster launch
+        // (scripts/tma_probe.cu, variant 1)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
     if (tid == 0) {
