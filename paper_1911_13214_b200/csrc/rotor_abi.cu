@@ -390,22 +390,122 @@ int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_ch
     if (!chains || !Ls || !limits || !costs || n_chains < 0 || n_limits < 0)
         return fail(ROTOR_EINPUT, "bad batch arguments");
     if (ops && (!ops_offsets || !ops_caps)) return fail(ROTOR_EINPUT, "ops requires ops_offsets and ops_caps");
-    int first_err = ROTOR_OK;
+    const int64_t P = (int64_t)n_chains * n_limits;
+    if (P == 0) return ROTOR_OK;
+    int L_max = 0;
     for (int i = 0; i < n_chains; i++) {
-        for (int j = 0; j < n_limits; j++) {
-            const int64_t pidx = (int64_t)i * n_limits + j;
-            int64_t cnt = 0;
-            rotor_op *o = ops ? ops + ops_offsets[pidx] : nullptr;
-            int64_t cap = ops ? ops_caps[pidx] : 0;
-            int r = rotor_solve_ex(&chains[i], Ls[i], limits[pidx], slots, opt, nullptr, 0, stream, &costs[pidx], o,
-                                   cap, &cnt);
-            if (status) status[pidx] = r;
-            if (n_ops) n_ops[pidx] = (r == ROTOR_OK || r == ROTOR_ETRUNC) ? cnt : -1;
-            if (r == ROTOR_INFEASIBLE) costs[pidx] = INFINITY;
-            if (r != ROTOR_OK && r != ROTOR_INFEASIBLE && r != ROTOR_ETRUNC && !first_err) first_err = r;
+        int r = check_args(Ls[i], 1, slots);
+        if (r) return r;
+        r = check_host_chain(&chains[i], Ls[i]);
+        if (r) return r;
+        L_max = std::max(L_max, (int)Ls[i]);
+    }
+    for (int64_t q = 0; q < P; q++)
+        if (limits[q] == 0) return fail(ROTOR_EINPUT, "mem_limit must be > 0 (problem %lld)", (long long)q);
+    const rotor_options o = opts_or_default(opt);
+    cudaStream_t st = (cudaStream_t)stream;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+
+    // host staging: chains padded to a common stride, problem descriptors
+    const int64_t stride = L_max + 2;
+    std::vector<double> h_d(2 * n_chains * stride, 0.0);
+    std::vector<uint64_t> h_u(5 * n_chains * stride, 0);
+    for (int i = 0; i < n_chains; i++) {
+        const int n1 = Ls[i] + 1;
+        memcpy(&h_d[(0 * n_chains + i) * stride], chains[i].uf, n1 * 8);
+        memcpy(&h_d[(1 * n_chains + i) * stride], chains[i].ub, n1 * 8);
+        memcpy(&h_u[(0 * n_chains + i) * stride], chains[i].wx, n1 * 8);
+        memcpy(&h_u[(1 * n_chains + i) * stride], chains[i].wbx, n1 * 8);
+        memcpy(&h_u[(2 * n_chains + i) * stride], chains[i].wy, (n1 + 1) * 8);
+        memcpy(&h_u[(3 * n_chains + i) * stride], chains[i].of, n1 * 8);
+        memcpy(&h_u[(4 * n_chains + i) * stride], chains[i].ob, n1 * 8);
+    }
+    std::vector<int32_t> h_pc(P), h_L(Ls, Ls + n_chains);
+    std::vector<int64_t> h_off(P, 0), h_cap(P, 0);
+    int64_t total_ops = 0;
+    for (int64_t q = 0; q < P; q++) {
+        h_pc[q] = (int32_t)(q / n_limits);
+        if (ops) {
+            h_cap[q] = std::max<int64_t>(0, ops_caps[q]);
+            h_off[q] = total_ops;
+            total_ops += h_cap[q];
         }
     }
-    return first_err;
+    const int n_slots = (int)std::min<int64_t>(P, 2 * (int64_t)sms);
+    const size_t slot = rotor::batch_slot_bytes(L_max, slots);
+    // one device allocation (library cache): descriptors, outputs, ops, then the slot pool
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t r = off;
+        off += al(bytes);
+        return r;
+    };
+    const size_t o_d = take(h_d.size() * 8), o_u = take(h_u.size() * 8), o_pc = take(P * 4), o_L = take(n_chains * 4),
+                 o_lim = take(P * 8), o_off = take(P * 8), o_cap = take(P * 8), o_cost = take(P * 8),
+                 o_nops = take(P * 8), o_st = take(P * 4), o_ops = take((size_t)std::max<int64_t>(total_ops, 1) * 8),
+                 o_ctr = take(8), o_pool = take((size_t)n_slots * slot);
+    void *wsv = nullptr;
+    int r = cached_workspace(off, &wsv);
+    if (r) return r;
+    char *w = (char *)wsv;
+    CK(cudaMemcpyAsync(w + o_d, h_d.data(), h_d.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_u, h_u.data(), h_u.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_pc, h_pc.data(), P * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_L, h_L.data(), n_chains * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_lim, limits, P * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_off, h_off.data(), P * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_cap, h_cap.data(), P * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(w + o_ctr, 0, 8, st));
+    rotor::BatchArgs b{};
+    b.n_problems = (int)P;
+    b.S = slots;
+    b.restricted = o.restricted ? 1 : 0;
+    b.L_max = L_max;
+    b.prob_chain = (const int32_t *)(w + o_pc);
+    b.limits = (const uint64_t *)(w + o_lim);
+    b.chain_L = (const int32_t *)(w + o_L);
+    b.chain_stride = stride;
+    b.uf = (const double *)(w + o_d);
+    b.ub = (const double *)(w + o_d) + n_chains * stride;
+    b.wx = (const uint64_t *)(w + o_u);
+    b.wbx = (const uint64_t *)(w + o_u) + 1 * n_chains * stride;
+    b.wy = (const uint64_t *)(w + o_u) + 2 * n_chains * stride;
+    b.of = (const uint64_t *)(w + o_u) + 3 * n_chains * stride;
+    b.ob = (const uint64_t *)(w + o_u) + 4 * n_chains * stride;
+    b.pool = w + o_pool;
+    b.cost = (double *)(w + o_cost);
+    b.nops = (int64_t *)(w + o_nops);
+    b.status = (int32_t *)(w + o_st);
+    b.ops = ops ? (rotor_op *)(w + o_ops) : nullptr;
+    b.ops_off = (const int64_t *)(w + o_off);
+    b.ops_cap = (const int64_t *)(w + o_cap);
+    b.counter = (int *)(w + o_ctr);
+    rotor::launch_batch(b, n_slots, st);
+    CK(cudaGetLastError());
+    std::vector<int64_t> h_n(P);
+    std::vector<int32_t> h_s(P);
+    CK(cudaMemcpyAsync(costs, w + o_cost, P * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_n.data(), w + o_nops, P * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_s.data(), w + o_st, P * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int first_err = ROTOR_OK;
+    for (int64_t q = 0; q < P; q++) {
+        int sq = h_s[q];
+        if (sq == ROTOR_OK && h_n[q] > h_cap[q] && ops) sq = ROTOR_ETRUNC;
+        if (status) status[q] = sq;
+        if (n_ops) n_ops[q] = (sq == ROTOR_OK || sq == ROTOR_ETRUNC) ? h_n[q] : -1;
+        if (sq == ROTOR_INFEASIBLE) costs[q] = INFINITY;
+        if (sq != ROTOR_OK && sq != ROTOR_INFEASIBLE && sq != ROTOR_ETRUNC && !first_err) first_err = sq;
+        if (ops && h_n[q] > 0 && h_cap[q] > 0) {
+            const int64_t cnt = std::min(h_n[q], h_cap[q]);
+            CK(cudaMemcpyAsync(ops + ops_offsets[q], w + o_ops + h_off[q] * 8, cnt * 8, cudaMemcpyDeviceToHost, st));
+        }
+    }
+    CK(cudaStreamSynchronize(st));
+    if (first_err) return fail(first_err, "batched solve: a problem failed with status %d", first_err);
+    return ROTOR_OK;
 }
 
 int rotor_partition_lpt(const double *weights, int32_t n_items, int32_t n_parts, int32_t *part_of) {

@@ -36,9 +36,14 @@ constexpr int TM = 16;      // m values per CTA (middle kernel)
 constexpr int STAGES = 3;   // TMA pipeline depth
 constexpr int THREADS = 256;
 constexpr int RS = 8, RT = 8;                 // register tile (s x t) per thread
+// A TMA box must start on a 16-byte boundary of the row (an odd fp64 start
+// column faults with "illegal instruction", scripts/tma_probe.cu): the shifted
+// C boxes start at the even column below the wanted one and are TMB = TM + 2
+// wide; the consumer adds the per-row offset (0 or 1).
+constexpr int TMB = TM + 2;
 constexpr int A_STAGE = TB * KC * TM;         // doubles [TB][KC][TM]
-constexpr int B_STAGE = KC * TB * TM;         // doubles [KC][TB][TM]
-constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * 8 + 64;
+constexpr int B_STAGE = KC * TB * TMB;        // doubles [KC][TB][TMB]
+constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * 8 + STAGES * 8 + STAGES * KC * 4 + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -85,8 +90,9 @@ __global__ void __launch_bounds__(THREADS, 1)
                   int delta) {
     extern __shared__ __align__(1024) double smem[];  // no static smem: the dynamic base is aligned
     double *As = smem;                       // [STAGES][TB][KC][TM]
-    double *Bs = smem + STAGES * A_STAGE;    // [STAGES][KC][TB][TM]
+    double *Bs = smem + STAGES * A_STAGE;    // [STAGES][KC][TB][TMB]
     uint64_t *bars = reinterpret_cast<uint64_t *>(Bs + STAGES * B_STAGE);
+    int *soff = reinterpret_cast<int *>(bars + STAGES);  // [STAGES][KC] column offset of each C box
 
     const int I = blockIdx.y, J = I + delta;
     const int i0 = I * TB + 1, j0 = J * TB + 1, i1 = i0 + TB;
@@ -99,6 +105,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int st = it % STAGES;
         const int sp0 = i1 + it * KC;
         uint64_t *bar = &bars[st];
+        // column offsets first: the expect_tx arrive (release) orders them
+        // before the consumers' barrier wait (acquire)
+        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - p.wx[sp0 + k - 1], -kPad) + kPad) & 1;
         mbar_expect_tx(bar, (uint32_t)((A_STAGE + B_STAGE) * 8));
         double *a_dst = As + st * A_STAGE;
         for (int a = 0; a < TB; a++) {
@@ -112,7 +121,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             // m = wx[sp-1] <= m_null(s,t): every cell it feeds is gated, so the
             // (clamped) values loaded for it are never used (DESIGN Q6).
             const int c0 = max(m0 - p.wx[sp - 1], -kPad) + kPad;
-            tma_load_2d(b_dst + k * TB * TM, &tmC, c0, (int)cell_index(n, sp, j0), bar);
+            tma_load_2d(b_dst + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp, j0), bar);
         }
     };
 
@@ -141,14 +150,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int st = it % STAGES;
         mbar_wait(&bars[st], (uint32_t)((it / STAGES) & 1));
         const double *a_s = As + st * A_STAGE + (sg * RS) * KC * TM + mi;
-        const double *b_s = Bs + st * B_STAGE + (tg * RT) * TM + mi;
+        const double *b_s = Bs + st * B_STAGE + (tg * RT) * TMB + mi;
 #pragma unroll
         for (int k = 0; k < KC; k++) {
             double a[RS], b[RT];
+            const double *bk = b_s + k * TB * TMB + soff[st * KC + k];
 #pragma unroll
             for (int i = 0; i < RS; i++) a[i] = a_s[i * KC * TM + k * TM];
 #pragma unroll
-            for (int j = 0; j < RT; j++) b[j] = b_s[k * TB * TM + j * TM];
+            for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
 #pragma unroll
             for (int i = 0; i < RS; i++)
 #pragma unroll
@@ -265,12 +275,12 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t pitch, int box_rows) {
+bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t pitch, int box_cols, int box_rows) {
     auto enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {(cuuint64_t)pitch, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)(pitch * 8)};
-    cuuint32_t box[2] = {(cuuint32_t)TM, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double *>(base), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -308,8 +318,8 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
     const int nb = (n + TB - 1) / TB;
     const int64_t rows = (int64_t)n * (n + 1) / 2;
     CUtensorMap tmA, tmC;  // over the whole allocations: left pad columns and spare rows included
-    if (!make_map(&tmA, p.A - kPad, rows + kPadRows, p.pitch, KC) ||
-        !make_map(&tmC, p.C - kPad, rows + kPadRows, p.pitch, TB))
+    if (!make_map(&tmA, p.A - kPad, rows + kPadRows, p.pitch, TM, KC) ||
+        !make_map(&tmC, p.C - kPad, rows + kPadRows, p.pitch, TMB, TB))
         return -1;
     const int dep_blocks = dep_grid_blocks();
     int launches = 0;

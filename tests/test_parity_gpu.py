@@ -183,6 +183,39 @@ def test_batched_equals_single(R, oracle_mod):
                 assert got == o.reconstruct()
 
 
+def test_config5_batched_sweep(R, oracle_mod):
+    """The full config-5 sweep (8 chains x 256 limits = 2048 tables) in one fused
+    launch: a seeded sample of 40 problems matches the oracle bit for bit (cost and
+    schedule); every feasible schedule replays valid within its limit with its cost."""
+    O = oracle_mod
+    chains, limits, S = G.config5()
+    costs, status, n_ops, ops = R.solve_batch(chains, limits, S, with_ops=True)
+    nl = len(limits[0])
+    rng = G.SplitMix64(5)
+    sample = {(rng.randint(0, len(chains) - 1), rng.randint(0, nl - 1)) for _ in range(40)}
+    for i, j in sorted(sample):
+        o = O.OracleSolve(chains[i], limits[i][j], S)
+        c = o.cost
+        if math.isinf(c):
+            assert status[i, j] == R.INFEASIBLE and math.isinf(costs[i, j])
+        else:
+            assert status[i, j] == R.OK and bits(np.array([costs[i, j]])) == bits(np.array([c]))
+            assert [tuple(map(int, r)) for r in ops[i * nl + j]] == o.reconstruct()
+    n_feasible = 0
+    for i, ch in enumerate(chains):
+        for j in range(nl):
+            if status[i, j] != R.OK:
+                assert status[i, j] == R.INFEASIBLE
+                continue
+            n_feasible += 1
+            sz = O.OracleSolve(ch, limits[i][j], S, fill=False).sizes()
+            seq = [tuple(map(int, r)) for r in ops[i * nl + j]]
+            rep = O.simulate(seq, sz, S)
+            assert rep.valid, (i, j, rep.failure)
+            assert abs(rep.makespan - costs[i, j]) <= len(seq) * math.ulp(costs[i, j])
+    assert n_feasible > 1000
+
+
 @pytest.mark.parametrize("kernel", KERNELS)
 def test_config3_full_table(R, oracle_mod, kernel):
     """DenseNet-shaped chain, L=300, S=2000 (9.2e9 transitions): full-table bit parity."""
