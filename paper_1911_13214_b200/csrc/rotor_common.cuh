@@ -51,6 +51,11 @@ __host__ __device__ inline int64_t cell_index(int n, int s, int t) {
     return r * n - r * (r - 1) / 2 + (t - s);
 }
 
+// Row of A(s,c) in the A table: column-major over the upper triangle
+// (c(c-1)/2 + s-1), so the cells (i0..i0+31, c) of one c — one TMA box of the
+// tiled middle kernel — are consecutive rows.
+__host__ __device__ inline int64_t a_index(int s, int c) { return (int64_t)c * (c - 1) / 2 + (s - 1); }
+
 __device__ __forceinline__ int m_all(const Problem &p, int s, int t) {
     // m_all(s,t) = max(wy[t] + wbx[s] + of[s], wy[s] + wbx[s] + ob[s])
     int a = p.wy[t] + p.wbx[s] + p.of[s];

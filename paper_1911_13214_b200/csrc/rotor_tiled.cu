@@ -2,18 +2,20 @@
 //
 // The split candidates of a cell (s,t) are
 //     cand(s') = fl( A(s, s'-1, m) + C(s', t, m - wx[s'-1]) ),  s' = s+1..t,
-// with A(s,c,m) = fl( fl(P[c] - P[s-1]) + C(s,c,m) ) stored next to C when a
-// cell is finalised (Q12 association: fl(fl(U + pre) + suf)).  For a fixed m
-// this is a min-plus product over s' (the m-shift depends on s' only), so the
-// triangle is cut into TB x TB tiles of (s,t), processed by tile diagonal
-// Delta = J - I.  For a tile (I,J), Delta >= 2:
-//   * middle: s' in blocks I+1..J-1 — every operand is final (shorter tile
-//     diagonals): a dense min-plus product with TB-fold operand reuse, operands
-//     streamed by TMA into shared memory (k_tile_middle);
-//   * dependent: s' in [s+1, i1-1] (B operand in this tile) and [j0, t]
-//     (A operand in this tile): finished in 2*TB-1 local anti-diagonal steps
-//     with a grid-wide barrier between steps (k_tile_dep, cooperative), which
-//     also applies the gates, the F_all candidate, and writes C and A.
+// with A(s,c,m) = fl( fl(P[c] - P[s-1]) + C(s,c,m) ) stored (column-major,
+// a_index) when a cell is finalised (Q12 association: fl(fl(U + pre) + suf)).
+// For a fixed m this is a min-plus product over s' (the m-shift depends on s'
+// only), so the triangle is cut into TB x TB tiles of (s,t), processed by tile
+// diagonal Delta = J - I.  For a tile (I,J):
+//   * middle (Delta >= 2): s' in blocks I+1..J-1 — every operand is final: a
+//     dense min-plus product with TB-fold operand reuse, operands streamed by
+//     TMA into shared memory through a full/empty mbarrier ring (k_tile_middle);
+//   * dependent: s' in [s+1, i1-1] (C operand in this tile, rows below) and
+//     [j0, t] (A operand in this tile, same row), the gates, F_all, and the
+//     writes of C and A — row by row from the bottom, a grid-wide barrier
+//     between rows (k_tile_dep, cooperative): a row only needs rows below at
+//     (shifted) lower m, which are complete, and its own earlier columns at the
+//     same m, which the same lane just computed (kept in shared memory).
 // Delta = 1 has no middle; Delta = 0 (diagonal tiles) is a local triangle.
 // The min is exact and every candidate has the fixed association above, so the
 // table is bit-identical to the wavefront / oracle fill (order-independent).
@@ -34,16 +36,17 @@ constexpr int TB = 32;      // tile edge in stages
 constexpr int KC = 8;       // splits per pipeline stage
 constexpr int TM = 16;      // m values per CTA (middle kernel)
 constexpr int STAGES = 3;   // TMA pipeline depth
-constexpr int THREADS = 256;
-constexpr int RS = 8, RT = 8;                 // register tile (s x t) per thread
+constexpr int CONSUMERS = 256;
+constexpr int THREADS = CONSUMERS;
+constexpr int RS = 8, RT = 8;            // register tile (s x t) per consumer thread
 // A TMA box must start on a 16-byte boundary of the row (an odd fp64 start
 // column faults with "illegal instruction", scripts/tma_probe.cu): the shifted
 // C boxes start at the even column below the wanted one and are TMB = TM + 2
 // wide; the consumer adds the per-row offset (0 or 1).
 constexpr int TMB = TM + 2;
-constexpr int A_STAGE = TB * KC * TM;         // doubles [TB][KC][TM]
-constexpr int B_STAGE = KC * TB * TMB;        // doubles [KC][TB][TMB]
-constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * 8 + STAGES * 8 + STAGES * KC * 4 + 64;
+constexpr int A_STAGE = KC * TB * TM;   // doubles [KC][TB s][TM]
+constexpr int B_STAGE = KC * TB * TMB;  // doubles [KC][TB t][TMB]
+constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * 8 + 2 * STAGES * 8 + STAGES * KC * 4 + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -56,6 +59,10 @@ __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
 __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
@@ -83,16 +90,19 @@ __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : 
 // ---------------------------------------------------------------------------
 // Middle phase of tile diagonal delta >= 2: partial(s,t,m) = min over s' in
 // blocks I+1..J-1 of A(s,s'-1,m) + C(s',t,m-wx[s'-1]); written into C.
-// grid = (ceil((S+1)/TM), tiles), block = 256; thread = one m, an 8x8 (s,t) tile.
+// grid = (ceil((S+1)/TM), tiles); 8 warps (thread = one m, an 8x8 (s,t)
+// register tile); thread 0 also issues the 16 TMA boxes of each stage
+// (full/empty mbarrier ring, no block-wide barrier in the main loop).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC, Problem p,
                   int delta) {
     extern __shared__ __align__(1024) double smem[];  // no static smem: the dynamic base is aligned
-    double *As = smem;                       // [STAGES][TB][KC][TM]
-    double *Bs = smem + STAGES * A_STAGE;    // [STAGES][KC][TB][TMB]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(Bs + STAGES * B_STAGE);
-    int *soff = reinterpret_cast<int *>(bars + STAGES);  // [STAGES][KC] column offset of each C box
+    double *As = smem;                     // [STAGES][KC][TB][TM]
+    double *Bs = smem + STAGES * A_STAGE;  // [STAGES][KC][TB][TMB]
+    uint64_t *full = reinterpret_cast<uint64_t *>(Bs + STAGES * B_STAGE);
+    uint64_t *empty = full + STAGES;
+    int *soff = reinterpret_cast<int *>(empty + STAGES);  // [STAGES][KC] column offset of each C box
 
     const int I = blockIdx.y, J = I + delta;
     const int i0 = I * TB + 1, j0 = J * TB + 1, i1 = i0 + TB;
@@ -100,42 +110,39 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int n = p.n;
     const int iters = (delta - 1) * TB / KC;
     const int tid = threadIdx.x;
+    const int lane = tid & 31;
 
+    // TMA producer: lane 0 of warp 0 (no dedicated warp: the 8x8 register tile
+    // needs ~240 registers, which leaves no room for a ninth warp)
     auto issue = [&](int it) {
         const int st = it % STAGES;
         const int sp0 = i1 + it * KC;
-        uint64_t *bar = &bars[st];
         // column offsets first: the expect_tx arrive (release) orders them
-        // before the consumers' barrier wait (acquire)
+        // before the consumers' full-barrier wait (acquire)
         for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - p.wx[sp0 + k - 1], -kPad) + kPad) & 1;
-        mbar_expect_tx(bar, (uint32_t)((A_STAGE + B_STAGE) * 8));
-        double *a_dst = As + st * A_STAGE;
-        for (int a = 0; a < TB; a++) {
-            const int s = i0 + a;  // cells (s, sp0-1 .. sp0+KC-2)
-            tma_load_2d(a_dst + a * KC * TM, &tmA, m0 + kPad, (int)cell_index(n, s, sp0 - 1), bar);
+        mbar_expect_tx(&full[st], (uint32_t)((A_STAGE + B_STAGE) * 8));
+        for (int k = 0; k < KC; k++) {  // A cells (i0..i0+TB-1, c), c = sp0+k-1
+            tma_load_2d(As + st * A_STAGE + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
         }
-        double *b_dst = Bs + st * B_STAGE;
-        for (int k = 0; k < KC; k++) {
-            const int sp = sp0 + k;  // cells (sp, j0 .. j0+TB-1) at m - wx[sp-1]
-            // A chunk whose shifted window starts below -kPad lies wholly under
-            // m = wx[sp-1] <= m_null(s,t): every cell it feeds is gated, so the
-            // (clamped) values loaded for it are never used (DESIGN Q6).
+        for (int k = 0; k < KC; k++) {  // C cells (sp, j0..j0+TB-1) at m - wx[sp-1]
+            const int sp = sp0 + k;
+            // a window starting below -kPad lies wholly under m = wx[sp-1] <= m_null(s,t):
+            // every cell it feeds is gated, the clamped values are never used (DESIGN Q6)
             const int c0 = max(m0 - p.wx[sp - 1], -kPad) + kPad;
-            tma_load_2d(b_dst + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp, j0), bar);
+            tma_load_2d(Bs + st * B_STAGE + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp, j0), &full[st]);
         }
     };
 
     if (tid == 0) {
-        for (int s = 0; s < STAGES; s++) mbar_init(&bars[s], 1);
-        // make the initialised barriers visible to the async (TMA) proxy; the
-        // .cluster-scoped fence.mbarrier_init faults in a non-cluster launch
-        // (scripts/tma_probe.cu, variant 1)
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CONSUMERS / 32);
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0)
         for (int it = 0; it < STAGES && it < iters; it++) issue(it);
-    }
 
     const int mi = tid & 15;
     const int g = tid >> 4;
@@ -148,15 +155,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     for (int it = 0; it < iters; it++) {
         const int st = it % STAGES;
-        mbar_wait(&bars[st], (uint32_t)((it / STAGES) & 1));
-        const double *a_s = As + st * A_STAGE + (sg * RS) * KC * TM + mi;
+        mbar_wait(&full[st], (uint32_t)((it / STAGES) & 1));
+        const double *a_s = As + st * A_STAGE + (sg * RS) * TM + mi;
         const double *b_s = Bs + st * B_STAGE + (tg * RT) * TMB + mi;
 #pragma unroll
         for (int k = 0; k < KC; k++) {
             double a[RS], b[RT];
             const double *bk = b_s + k * TB * TMB + soff[st * KC + k];
 #pragma unroll
-            for (int i = 0; i < RS; i++) a[i] = a_s[i * KC * TM + k * TM];
+            for (int i = 0; i < RS; i++) a[i] = a_s[k * TB * TM + i * TM];
 #pragma unroll
             for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
 #pragma unroll
@@ -164,8 +171,12 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
         }
-        __syncthreads();  // every thread is done reading stage st
-        if (tid == 0 && it + STAGES < iters) issue(it + STAGES);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading stage st
+        if (tid == 0 && it + STAGES < iters) {   // refill st once all 8 warps released it
+            mbar_wait(&empty[st], (uint32_t)((it / STAGES) & 1));
+            issue(it + STAGES);
+        }
     }
 
     const int m = m0 + mi;
@@ -183,44 +194,84 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Dependent phase of tile diagonal delta (cooperative; grid-wide barrier
-// between the local anti-diagonal steps).  One warp = one cell x 32 m values.
+// Dependent phase (cooperative; grid-wide barrier between tile rows).
+// One warp = one tile row x 32 consecutive m; the lane walks the row's cells
+// left to right, keeping the row's A values in registers.  Values written in
+// earlier rows of this launch (other CTAs) are read with ld.global.cg;
+// values of earlier launches with plain (L1-cached) loads.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void finish_cell(const Problem &p, const double *A, double *Aw, int s, int t, int m,
-                                            int lo1, int hi1, int lo2, int hi2, bool partial) {
+__device__ __forceinline__ double gate_and_store(const Problem &p, int s, int t, int m, double c1) {
     const int n = p.n;
     const int64_t pitch = p.pitch;
-    const int64_t cst = cell_index(n, s, t);
-    // Values written by other CTAs in earlier steps of this launch are read with
-    // ld.global.cg (L2, never a stale L1 line).
-    double c1 = INFINITY;
-    if (m >= m_null(p, s, t)) {
-        double best = partial ? __ldcg(&p.C[cst * pitch + m]) : INFINITY;
-        const int64_t rs = cell_index(n, s, s);  // A(s, c) at row rs + (c - s)
-        for (int sp = lo1; sp <= hi1; sp++) {
-            const int mm = m - p.wx[sp - 1];  // >= 0 under the m_null gate (DESIGN Q6)
-            const double v = __dadd_rn(__ldcg(&A[(rs + (sp - 1 - s)) * pitch + m]),
-                                       __ldcg(&p.C[cell_index(n, sp, t) * pitch + mm]));
-            best = dmin(best, v);
-        }
-        for (int sp = lo2; sp <= hi2; sp++) {
-            const int mm = m - p.wx[sp - 1];
-            const double v = __dadd_rn(__ldcg(&A[(rs + (sp - 1 - s)) * pitch + m]),
-                                       __ldcg(&p.C[cell_index(n, sp, t) * pitch + mm]));
-            best = dmin(best, v);
-        }
-        c1 = best;
-    }
     double c = c1;
-    if (!p.restricted && m >= m_all(p, s, t)) {  // m - wbx[s] >= 0 under the m_all gate
+    if (!p.restricted && m >= m_all(p, s, t)) {  // m - wbx[s] >= 0 under the gate; row s+1 done earlier
         const double v = __dadd_rn(p.w[s], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - p.wbx[s])]));
         c = dmin(c, v);
     }
-    p.C[cst * pitch + m] = c;
-    if (t < n) Aw[cst * pitch + m] = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), c);
+    p.C[cell_index(n, s, t) * pitch + m] = c;
+    const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), c);
+    if (t < n) p.A[a_index(s, t) * pitch + m] = a;
+    return a;
 }
 
-__global__ void __launch_bounds__(256) k_tile_dep(Problem p, double *A, int delta, int partial) {
+constexpr int DEP_THREADS = 128;
+
+// Row s of an off-diagonal tile (I,J), delta >= 1.  AR (shared memory, one
+// column per thread) holds AR[c'] = A(s, j0 + c' - 1), the right-range A
+// operands of this row, as the row is computed.
+__device__ __forceinline__ void dep_row_off(const Problem &p, int s, int i1, int j0, int m, bool partial,
+                                            double *AR) {
+    const int n = p.n;
+    const int64_t pitch = p.pitch;
+    AR[0] = p.A[a_index(s, j0 - 1) * pitch + m];
+    for (int c = 0; c < TB; c++) {
+        const int t = j0 + c;
+        if (t > n) break;
+        double c1 = INFINITY;
+        if (m >= m_null(p, s, t)) {  // every shifted index below is >= 0 under this gate (DESIGN Q6)
+            double best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
+            for (int sp = s + 1; sp < i1; sp++) {  // left range: C in rows below (this launch)
+                const double av = p.A[a_index(s, sp - 1) * pitch + m];
+                best = dmin(best, __dadd_rn(av, __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])])));
+            }
+            for (int cp = 0; cp <= c; cp++) {  // right range s' = j0 + cp: C in tile (J,J) (earlier launch)
+                const int sp = j0 + cp;
+                best = dmin(best, __dadd_rn(AR[cp * DEP_THREADS],
+                                            p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])]));
+            }
+            c1 = best;
+        }
+        AR[(c + 1) * DEP_THREADS] = gate_and_store(p, s, t, m, c1);
+    }
+}
+
+// Row s of a diagonal tile (delta = 0): cells (s, s+1..i0+TB-1), splits s' in (s, t];
+// AD[c] = A(s, i0 + c) (shared memory, one column per thread).
+__device__ __forceinline__ void dep_row_diag(const Problem &p, int s, int i0, int m, double *AD) {
+    const int n = p.n;
+    const int64_t pitch = p.pitch;
+    const int a = s - i0;
+    AD[a * DEP_THREADS] = p.A[a_index(s, s) * pitch + m];  // the leaf (written by k_leaf)
+    for (int c = a + 1; c < TB; c++) {
+        const int t = i0 + c;
+        if (t > n) break;
+        double c1 = INFINITY;
+        if (m >= m_null(p, s, t)) {
+            double best = INFINITY;
+            for (int cp = a; cp < c; cp++) {  // s' = i0 + cp + 1, A(s, s'-1) = AD[cp]
+                const int sp = i0 + cp + 1;
+                best = dmin(best, __dadd_rn(AD[cp * DEP_THREADS],
+                                            __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])])));
+            }
+            c1 = best;
+        }
+        AD[c * DEP_THREADS] = gate_and_store(p, s, t, m, c1);
+    }
+}
+
+__global__ void __launch_bounds__(DEP_THREADS) k_tile_dep(Problem p, int delta, int partial) {
+    __shared__ double rowA[(TB + 1) * DEP_THREADS];
+    double *myA = rowA + threadIdx.x;
     cg::grid_group grid = cg::this_grid();
     const int n = p.n, S = p.S;
     const int nb = (n + TB - 1) / TB;
@@ -229,32 +280,19 @@ __global__ void __launch_bounds__(256) k_tile_dep(Problem p, double *A, int delt
     const int lane = threadIdx.x & 31;
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int e_lo = delta == 0 ? 1 : 0;
-    const int e_hi = delta == 0 ? TB - 1 : 2 * TB - 2;
-    for (int e = e_lo; e <= e_hi; e++) {
-        // cells of local step e in one tile
-        const int a_lo = delta == 0 ? 0 : max(0, (TB - 1) - e);
-        const int a_hi = delta == 0 ? TB - 1 - e : min(TB - 1, 2 * TB - 2 - e);
-        const int cnt = a_hi - a_lo + 1;
-        const long long items = (long long)ntiles * cnt * n_mg;
-        for (long long item = warp; item < items; item += nwarps) {
-            const int mg = (int)(item % n_mg);
-            const long long rest = item / n_mg;
-            const int q = (int)(rest % cnt);
-            const int I = (int)(rest / cnt);
-            const int J = I + delta;
-            const int a = a_lo + q;
-            const int i0 = I * TB + 1, j0 = J * TB + 1;
+    const int items = ntiles * n_mg;
+    for (int a = TB - 1; a >= 0; a--) {
+        for (int item = warp; item < items; item += nwarps) {
+            const int mg = item % n_mg;
+            const int I = item / n_mg;
+            const int i0 = I * TB + 1;
             const int s = i0 + a;
-            const int t = delta == 0 ? s + e : j0 + (a + e - (TB - 1));
             const int m = mg * 32 + lane;
-            if (s > n || t > n || m > S) continue;
-            if (delta == 0) {
-                finish_cell(p, A, A, s, t, m, s + 1, t, 1, 0, false);
-            } else {
-                const int i1 = i0 + TB;
-                finish_cell(p, A, A, s, t, m, s + 1, min(t, i1 - 1), j0, t, partial != 0);
-            }
+            if (s > n || m > S) continue;
+            if (delta == 0)
+                dep_row_diag(p, s, i0, m, myA);
+            else
+                dep_row_off(p, s, i0 + TB, (I + delta) * TB + 1, m, partial != 0, myA);
         }
         grid.sync();
     }
@@ -294,7 +332,7 @@ int dep_grid_blocks() {
         int dev = 0, sms = 0, per = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_dep, 256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_dep, DEP_THREADS, 0);
         blocks = sms * (per > 0 ? per : 1);
     }
     return blocks;
@@ -318,7 +356,7 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
     const int nb = (n + TB - 1) / TB;
     const int64_t rows = (int64_t)n * (n + 1) / 2;
     CUtensorMap tmA, tmC;  // over the whole allocations: left pad columns and spare rows included
-    if (!make_map(&tmA, p.A - kPad, rows + kPadRows, p.pitch, TM, KC) ||
+    if (!make_map(&tmA, p.A - kPad, rows + kPadRows, p.pitch, TM, TB) ||
         !make_map(&tmC, p.C - kPad, rows + kPadRows, p.pitch, TMB, TB))
         return -1;
     const int dep_blocks = dep_grid_blocks();
@@ -330,10 +368,10 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
             launches++;
         }
         Problem pp = p;
-        double *A = p.A;
         int d = delta, part = delta >= 2 ? 1 : 0;
-        void *args[] = {&pp, &A, &d, &part};
-        if (cudaLaunchCooperativeKernel((void *)k_tile_dep, dim3(dep_blocks), dim3(256), args, 0, st) != cudaSuccess)
+        void *args[] = {&pp, &d, &part};
+        if (cudaLaunchCooperativeKernel((void *)k_tile_dep, dim3(dep_blocks), dim3(DEP_THREADS), args, 0, st) !=
+            cudaSuccess)
             return -1;
         launches++;
     }
