@@ -230,14 +230,43 @@ __device__ __forceinline__ void dep_row_off(const Problem &p, int s, int i1, int
         double c1 = INFINITY;
         if (m >= m_null(p, s, t)) {  // every shifted index below is >= 0 under this gate (DESIGN Q6)
             double best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
-            for (int sp = s + 1; sp < i1; sp++) {  // left range: C in rows below (this launch)
-                const double av = p.A[a_index(s, sp - 1) * pitch + m];
-                best = dmin(best, __dadd_rn(av, __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])])));
+            // left range s' = s+1..i1-1: C in rows below (this launch: L2), A(s, s'-1) of tile (I,I)
+            // (earlier launch: L1-cached, the same row for every c); batches of 8 loads in flight
+            {
+                int64_t crow = cell_index(n, s + 1, t);
+                for (int sp0 = s + 1; sp0 < i1; sp0 += 8) {
+                    double cv[8], av[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        const int sp = sp0 + u;
+                        if (sp < i1) {
+                            cv[u] = __ldcg(&p.C[crow * pitch + (m - p.wx[sp - 1])]);
+                            av[u] = p.A[a_index(s, sp - 1) * pitch + m];
+                            crow += n - sp;  // cell(sp+1, t) - cell(sp, t)
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u++)
+                        if (sp0 + u < i1) best = dmin(best, __dadd_rn(av[u], cv[u]));
+                }
             }
-            for (int cp = 0; cp <= c; cp++) {  // right range s' = j0 + cp: C in tile (J,J) (earlier launch)
-                const int sp = j0 + cp;
-                best = dmin(best, __dadd_rn(AR[cp * DEP_THREADS],
-                                            p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])]));
+            // right range s' = j0..t: C in tile (J,J) (earlier launch), A(s, s'-1) = AR (this row)
+            {
+                int64_t crow = cell_index(n, j0, t);
+                for (int cp0 = 0; cp0 <= c; cp0 += 8) {
+                    double cv[8];
+#pragma unroll
+                    for (int u = 0; u < 8; u++) {
+                        const int sp = j0 + cp0 + u;
+                        if (cp0 + u <= c) {
+                            cv[u] = p.C[crow * pitch + (m - p.wx[sp - 1])];
+                            crow += n - sp;
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u++)
+                        if (cp0 + u <= c) best = dmin(best, __dadd_rn(AR[(cp0 + u) * DEP_THREADS], cv[u]));
+                }
             }
             c1 = best;
         }
@@ -258,10 +287,20 @@ __device__ __forceinline__ void dep_row_diag(const Problem &p, int s, int i0, in
         double c1 = INFINITY;
         if (m >= m_null(p, s, t)) {
             double best = INFINITY;
-            for (int cp = a; cp < c; cp++) {  // s' = i0 + cp + 1, A(s, s'-1) = AD[cp]
-                const int sp = i0 + cp + 1;
-                best = dmin(best, __dadd_rn(AD[cp * DEP_THREADS],
-                                            __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])])));
+            int64_t crow = cell_index(n, s + 1, t);
+            for (int cp0 = a; cp0 < c; cp0 += 8) {  // s' = i0 + cp + 1, A(s, s'-1) = AD[cp]
+                double cv[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int sp = i0 + cp0 + u + 1;
+                    if (cp0 + u < c) {
+                        cv[u] = __ldcg(&p.C[crow * pitch + (m - p.wx[sp - 1])]);
+                        crow += n - sp;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+                    if (cp0 + u < c) best = dmin(best, __dadd_rn(AD[(cp0 + u) * DEP_THREADS], cv[u]));
             }
             c1 = best;
         }
