@@ -35,8 +35,8 @@ sys.path.insert(0, ROOT)
 
 METRIC = "DP cell-transitions/sec and solve time (L=1000, 4000 slots); % HBM roofline"
 UNIT = "transitions/s"
-REF_WINDOW = 150  # stages in the oracle's bounded sample (reference arm steps)
-CPU_BASELINE_WINDOW = 180  # stages in the cpu_baseline sample (~10-20 s single-thread)
+REF_WINDOW = int(os.environ.get("ROTOR_REF_WINDOW", 150))  # stages in the reference arm's bounded sample
+CPU_BASELINE_WINDOW = int(os.environ.get("ROTOR_CPU_WINDOW", 180))  # cpu_baseline sample (~10-20 s single-thread)
 
 
 def parse():

@@ -12,22 +12,19 @@
 //     TMA into shared memory through a full/empty mbarrier ring (k_tile_middle);
 //   * dependent: s' in [s+1, i1-1] (C operand in this tile, rows below) and
 //     [j0, t] (A operand in this tile, same row), the gates, F_all, and the
-//     writes of C and A — row by row from the bottom, a grid-wide barrier
-//     between rows (k_tile_dep, cooperative): a row only needs rows below at
-//     (shifted) lower m, which are complete, and its own earlier columns at the
-//     same m, which the same lane just computed (kept in shared memory).
+//     writes of C and A — a second tiling level of SB x SB sub-tiles
+//     (rotor_tiled_dep.cuh): sub-products with SB-fold reuse, then short
+//     row-by-row leaves; a row only needs rows below at (shifted) lower m,
+//     which are complete, and its own earlier columns at the same m.
 // Delta = 1 has no middle; Delta = 0 (diagonal tiles) is a local triangle.
 // The min is exact and every candidate has the fixed association above, so the
 // table is bit-identical to the wavefront / oracle fill (order-independent).
-#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math.h>
 
 #include "rotor_common.cuh"
 #include "rotor_kernels.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace rotor {
 namespace tiled {
@@ -193,149 +190,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-// ---------------------------------------------------------------------------
-// Dependent phase (cooperative; grid-wide barrier between tile rows).
-// One warp = one tile row x 32 consecutive m; the lane walks the row's cells
-// left to right, keeping the row's A values in registers.  Values written in
-// earlier rows of this launch (other CTAs) are read with ld.global.cg;
-// values of earlier launches with plain (L1-cached) loads.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ double gate_and_store(const Problem &p, int s, int t, int m, double c1) {
-    const int n = p.n;
-    const int64_t pitch = p.pitch;
-    double c = c1;
-    if (!p.restricted && m >= m_all(p, s, t)) {  // m - wbx[s] >= 0 under the gate; row s+1 done earlier
-        const double v = __dadd_rn(p.w[s], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - p.wbx[s])]));
-        c = dmin(c, v);
-    }
-    p.C[cell_index(n, s, t) * pitch + m] = c;
-    const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), c);
-    if (t < n) p.A[a_index(s, t) * pitch + m] = a;
-    return a;
-}
-
-constexpr int DEP_THREADS = 128;
-
-// Row s of an off-diagonal tile (I,J), delta >= 1.  AR (shared memory, one
-// column per thread) holds AR[c'] = A(s, j0 + c' - 1), the right-range A
-// operands of this row, as the row is computed.
-__device__ __forceinline__ void dep_row_off(const Problem &p, int s, int i1, int j0, int m, bool partial,
-                                            double *AR) {
-    const int n = p.n;
-    const int64_t pitch = p.pitch;
-    AR[0] = p.A[a_index(s, j0 - 1) * pitch + m];
-    for (int c = 0; c < TB; c++) {
-        const int t = j0 + c;
-        if (t > n) break;
-        double c1 = INFINITY;
-        if (m >= m_null(p, s, t)) {  // every shifted index below is >= 0 under this gate (DESIGN Q6)
-            double best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
-            // left range s' = s+1..i1-1: C in rows below (this launch: L2), A(s, s'-1) of tile (I,I)
-            // (earlier launch: L1-cached, the same row for every c); batches of 8 loads in flight
-            {
-                int64_t crow = cell_index(n, s + 1, t);
-                for (int sp0 = s + 1; sp0 < i1; sp0 += 8) {
-                    double cv[8], av[8];
-#pragma unroll
-                    for (int u = 0; u < 8; u++) {
-                        const int sp = sp0 + u;
-                        if (sp < i1) {
-                            cv[u] = __ldcg(&p.C[crow * pitch + (m - p.wx[sp - 1])]);
-                            av[u] = p.A[a_index(s, sp - 1) * pitch + m];
-                            crow += n - sp;  // cell(sp+1, t) - cell(sp, t)
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; u++)
-                        if (sp0 + u < i1) best = dmin(best, __dadd_rn(av[u], cv[u]));
-                }
-            }
-            // right range s' = j0..t: C in tile (J,J) (earlier launch), A(s, s'-1) = AR (this row)
-            {
-                int64_t crow = cell_index(n, j0, t);
-                for (int cp0 = 0; cp0 <= c; cp0 += 8) {
-                    double cv[8];
-#pragma unroll
-                    for (int u = 0; u < 8; u++) {
-                        const int sp = j0 + cp0 + u;
-                        if (cp0 + u <= c) {
-                            cv[u] = p.C[crow * pitch + (m - p.wx[sp - 1])];
-                            crow += n - sp;
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < 8; u++)
-                        if (cp0 + u <= c) best = dmin(best, __dadd_rn(AR[(cp0 + u) * DEP_THREADS], cv[u]));
-                }
-            }
-            c1 = best;
-        }
-        AR[(c + 1) * DEP_THREADS] = gate_and_store(p, s, t, m, c1);
-    }
-}
-
-// Row s of a diagonal tile (delta = 0): cells (s, s+1..i0+TB-1), splits s' in (s, t];
-// AD[c] = A(s, i0 + c) (shared memory, one column per thread).
-__device__ __forceinline__ void dep_row_diag(const Problem &p, int s, int i0, int m, double *AD) {
-    const int n = p.n;
-    const int64_t pitch = p.pitch;
-    const int a = s - i0;
-    AD[a * DEP_THREADS] = p.A[a_index(s, s) * pitch + m];  // the leaf (written by k_leaf)
-    for (int c = a + 1; c < TB; c++) {
-        const int t = i0 + c;
-        if (t > n) break;
-        double c1 = INFINITY;
-        if (m >= m_null(p, s, t)) {
-            double best = INFINITY;
-            int64_t crow = cell_index(n, s + 1, t);
-            for (int cp0 = a; cp0 < c; cp0 += 8) {  // s' = i0 + cp + 1, A(s, s'-1) = AD[cp]
-                double cv[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int sp = i0 + cp0 + u + 1;
-                    if (cp0 + u < c) {
-                        cv[u] = __ldcg(&p.C[crow * pitch + (m - p.wx[sp - 1])]);
-                        crow += n - sp;
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < 8; u++)
-                    if (cp0 + u < c) best = dmin(best, __dadd_rn(AD[(cp0 + u) * DEP_THREADS], cv[u]));
-            }
-            c1 = best;
-        }
-        AD[c * DEP_THREADS] = gate_and_store(p, s, t, m, c1);
-    }
-}
-
-__global__ void __launch_bounds__(DEP_THREADS) k_tile_dep(Problem p, int delta, int partial) {
-    __shared__ double rowA[(TB + 1) * DEP_THREADS];
-    double *myA = rowA + threadIdx.x;
-    cg::grid_group grid = cg::this_grid();
-    const int n = p.n, S = p.S;
-    const int nb = (n + TB - 1) / TB;
-    const int ntiles = nb - delta;
-    const int n_mg = (S + 1 + 31) / 32;
-    const int lane = threadIdx.x & 31;
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nwarps = (gridDim.x * blockDim.x) >> 5;
-    const int items = ntiles * n_mg;
-    for (int a = TB - 1; a >= 0; a--) {
-        for (int item = warp; item < items; item += nwarps) {
-            const int mg = item % n_mg;
-            const int I = item / n_mg;
-            const int i0 = I * TB + 1;
-            const int s = i0 + a;
-            const int m = mg * 32 + lane;
-            if (s > n || m > S) continue;
-            if (delta == 0)
-                dep_row_diag(p, s, i0, m, myA);
-            else
-                dep_row_off(p, s, i0 + TB, (I + delta) * TB + 1, m, partial != 0, myA);
-        }
-        grid.sync();
-    }
-}
+#include "rotor_tiled_dep.cuh"
 
 // ---------------------------------------------------------------------------
 // host side
@@ -365,18 +220,6 @@ bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t pitch,
     return r == CUDA_SUCCESS;
 }
 
-int dep_grid_blocks() {
-    static int blocks = 0;
-    if (!blocks) {
-        int dev = 0, sms = 0, per = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_tile_dep, DEP_THREADS, 0);
-        blocks = sms * (per > 0 ? per : 1);
-    }
-    return blocks;
-}
-
 }  // namespace tiled
 
 size_t tiled_extra_bytes(int, int) { return 0; }  // the A table is part of the Layout (rotor_abi.cu)
@@ -398,7 +241,6 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
     if (!make_map(&tmA, p.A - kPad, rows + kPadRows, p.pitch, TM, TB) ||
         !make_map(&tmC, p.C - kPad, rows + kPadRows, p.pitch, TMB, TB))
         return -1;
-    const int dep_blocks = dep_grid_blocks();
     int launches = 0;
     for (int delta = 0; delta < nb; delta++) {
         if (delta >= 2) {
@@ -406,13 +248,7 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
             k_tile_middle<<<grid, THREADS, SMEM_BYTES, st>>>(tmA, tmC, p, delta);
             launches++;
         }
-        Problem pp = p;
-        int d = delta, part = delta >= 2 ? 1 : 0;
-        void *args[] = {&pp, &d, &part};
-        if (cudaLaunchCooperativeKernel((void *)k_tile_dep, dim3(dep_blocks), dim3(DEP_THREADS), args, 0, st) !=
-            cudaSuccess)
-            return -1;
-        launches++;
+        launches += launch_dependent(p, delta, st);
     }
     return launches;
 }

@@ -1,0 +1,254 @@
+// Dependent phase of the tiled fill — two-level (included by rotor_tiled.cu
+// inside namespace rotor::tiled).
+//
+// Inside a TB x TB tile (I,J) the splits that need values of the tile itself
+// are s' in [s+1, i1-1] (left: C of rows below) and [j0, t] (right: A of the
+// same row).  Cut the tile into NSB x NSB sub-tiles of SB x SB cells, (alpha,
+// gamma) = (row sub-block of I, column sub-block of J).  Sub-tile (alpha,gamma)
+// depends on sub-tiles (alpha' > alpha, gamma) and (alpha, gamma' < gamma), so
+// sub-tiles are processed by sub-anti-diagonal eps = gamma - alpha + NSB-1;
+// for each sub-tile
+//   * product: the left splits in sub-blocks alpha+1.. of I and the right
+//     splits in sub-blocks ..gamma-1 of J, whose operands are final: an SB x SB
+//     min-plus product per m (8x8 register tile per lane), min-ed into the
+//     partial value held in C (k_sub_product);
+//   * leaf: the splits inside its own row sub-block / column sub-block, the
+//     gates, F_all, and the writes of C and A, one local row per launch from
+//     the bottom (k_sub_leaf): a row needs the rows below (complete, at
+//     shifted m) and its own earlier columns at the same m (registers).
+// Diagonal tiles (Delta = 0) use the same scheme with sub-diagonals
+// delta' = gamma - alpha = 0..NSB-1 (products for delta' >= 2).
+// Only cells x SB x (S+1) transitions remain in the leaves (vs cells x TB);
+// the rest runs as products with SB-fold register reuse.
+
+constexpr int SB = 8;
+constexpr int NSB = TB / SB;
+constexpr int DEP_THREADS = 128;
+
+// number of sub-tiles of phase e, and the q-th one
+__host__ __device__ inline int sub_count(int delta, int e) {
+    return delta == 0 ? NSB - e : NSB - (e >= NSB - 1 ? e - (NSB - 1) : (NSB - 1) - e);
+}
+__host__ __device__ inline void sub_at(int delta, int e, int q, int &alpha, int &gamma) {
+    if (delta == 0) {
+        alpha = q;
+        gamma = q + e;
+    } else {
+        const int dd = e - (NSB - 1);  // gamma - alpha
+        alpha = (dd >= 0 ? 0 : -dd) + q;
+        gamma = alpha + dd;
+    }
+}
+
+// C / A loads: `fresh` = written earlier in this launch sequence of the same
+// tile diagonal (another CTA, earlier kernel of this Delta) -> L2 (.cg);
+// otherwise written by an earlier tile diagonal -> plain (L1-cacheable).
+__device__ __forceinline__ double ld(const double *p, bool fresh) { return fresh ? __ldcg(p) : *p; }
+
+// Product for one sub-tile, one m (lane), an SB x SB register tile.
+__global__ void __launch_bounds__(DEP_THREADS) k_sub_product(Problem p, int delta, int e) {
+    const int n = p.n, S = p.S;
+    const int nb = (n + TB - 1) / TB;
+    const int ntiles = nb - delta;
+    const int cnt = sub_count(delta, e);
+    const int n_mg = (S + 1 + 31) / 32;
+    const int item = (blockIdx.x * DEP_THREADS + threadIdx.x) >> 5;
+    if (item >= ntiles * cnt * n_mg) return;
+    const int m = (item % n_mg) * 32 + (threadIdx.x & 31);
+    const int rest = item / n_mg;
+    int alpha, gamma;
+    sub_at(delta, e, rest % cnt, alpha, gamma);
+    const int I = rest / cnt, J = I + delta;
+    const int i0 = I * TB + 1, j0 = J * TB + 1;
+    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
+    // split ranges and the freshness of their operands
+    int lo1, hi1, lo2 = 1, hi2 = 0;
+    bool fA1, fC1, fA2 = true, fC2 = true, partial;
+    if (delta == 0) {  // sub-blocks alpha+1 .. gamma-1, all inside this tile
+        lo1 = i0 + SB * (alpha + 1);
+        hi1 = t0 - 1;
+        fA1 = fC1 = true;
+        partial = false;
+    } else {
+        lo1 = s0 + SB;  // sub-blocks alpha+1 .. NSB-1 of I
+        hi1 = i0 + TB - 1;
+        fA1 = false;  // A(s, s'-1) in tile (I,I)
+        fC1 = true;   // C(s', t) in this tile
+        lo2 = j0;     // sub-blocks 0 .. gamma-1 of J
+        hi2 = t0 - 1;
+        fA2 = true;   // A(s, s'-1) in this tile (or (I,J-1) for s' = j0: earlier, .cg is still correct)
+        fC2 = false;  // C(s', t) in tile (J,J)
+        partial = delta >= 2;
+    }
+    if (hi1 < lo1 && hi2 < lo2) return;
+    if (m > S) return;
+    const int64_t pitch = p.pitch;
+    double acc[SB][SB];
+#pragma unroll
+    for (int i = 0; i < SB; i++)
+#pragma unroll
+        for (int j = 0; j < SB; j++) {
+            const int s = s0 + i, t = t0 + j;
+            acc[i][j] = (partial && s <= n && t <= n) ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
+        }
+    for (int r = 0; r < 2; r++) {
+        const int lo = r ? lo2 : lo1, hi = r ? hi2 : hi1;
+        const bool fA = r ? fA2 : fA1, fC = r ? fC2 : fC1;
+        for (int sp = lo; sp <= hi; sp++) {
+            const int w = p.wx[sp - 1];
+            if (m < w) continue;  // every cell this candidate feeds is gated (m < w <= m_null)
+            const double *ap = p.A + a_index(s0, sp - 1) * pitch + m;  // A(s0+i, sp-1): consecutive rows
+            const double *cp = p.C + cell_index(n, sp, t0) * pitch + (m - w);  // C(sp, t0+j): consecutive rows
+            double a[SB], c[SB];
+#pragma unroll
+            for (int i = 0; i < SB; i++) a[i] = (s0 + i <= n) ? ld(ap + i * pitch, fA) : INFINITY;
+#pragma unroll
+            for (int j = 0; j < SB; j++) c[j] = (t0 + j <= n) ? ld(cp + j * pitch, fC) : INFINITY;
+#pragma unroll
+            for (int i = 0; i < SB; i++)
+#pragma unroll
+                for (int j = 0; j < SB; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], c[j]));
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < SB; i++)
+#pragma unroll
+        for (int j = 0; j < SB; j++) {
+            const int s = s0 + i, t = t0 + j;
+            if (s <= n && t <= n) p.C[cell_index(n, s, t) * pitch + m] = acc[i][j];
+        }
+}
+
+// Finish cell (s,t) at m from its running minimum c1 (already gated): F_all
+// candidate, store C and A; returns A(s,t,m).
+__device__ __forceinline__ double finish(const Problem &p, int s, int t, int m, double c1) {
+    const int n = p.n;
+    const int64_t pitch = p.pitch;
+    double c = c1;
+    if (!p.restricted && m >= m_all(p, s, t)) {  // m - wbx[s] >= 0 under the gate; row s+1 is final
+        const double v = __dadd_rn(p.w[s], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - p.wbx[s])]));
+        c = dmin(c, v);
+    }
+    p.C[cell_index(n, s, t) * pitch + m] = c;
+    const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), c);
+    if (t < n) p.A[a_index(s, t) * pitch + m] = a;
+    return a;
+}
+
+// Leaf: local row r of every sub-tile of phase e.  The lane walks the row's
+// SB cells left to right; right-range A operands of the row stay in registers.
+__global__ void __launch_bounds__(DEP_THREADS) k_sub_leaf(Problem p, int delta, int e, int r) {
+    const int n = p.n, S = p.S;
+    const int nb = (n + TB - 1) / TB;
+    const int ntiles = nb - delta;
+    const int cnt = sub_count(delta, e);
+    const int n_mg = (S + 1 + 31) / 32;
+    const int item = (blockIdx.x * DEP_THREADS + threadIdx.x) >> 5;
+    if (item >= ntiles * cnt * n_mg) return;
+    const int m = (item % n_mg) * 32 + (threadIdx.x & 31);
+    const int rest = item / n_mg;
+    int alpha, gamma;
+    sub_at(delta, e, rest % cnt, alpha, gamma);
+    const int I = rest / cnt, J = I + delta;
+    const int i0 = I * TB + 1, j0 = J * TB + 1;
+    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
+    const int s = s0 + r;
+    const int ea = s0 + SB - 1;  // last row of this row sub-block
+    if (s > n || m > S) return;
+    const int64_t pitch = p.pitch;
+    double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
+
+    if (delta == 0 && e == 0) {  // diagonal sub-tile: cells (s, s+1..ea), splits s' in (s, t]
+        const double leaf = p.A[a_index(s, s) * pitch + m];  // the leaf (k_leaf, an earlier launch)
+#pragma unroll
+        for (int c = 0; c < SB; c++)  // AR[r + 1] = leaf, with compile-time register indices
+            if (c == r) AR[c + 1] = leaf;
+#pragma unroll
+        for (int c = 0; c < SB; c++) {
+            if (c <= r) continue;
+            const int t = t0 + c;
+            if (t > n) break;
+            double c1 = INFINITY;
+            if (m >= m_null(p, s, t)) {  // every shifted index is >= 0 under this gate (DESIGN Q6)
+                double best = INFINITY;
+#pragma unroll
+                for (int cq = 0; cq < SB; cq++) {  // s' = t0 + cq + 1 in (s, t]
+                    if (cq < r || cq >= c) continue;
+                    const int sp = t0 + cq + 1;
+                    const double cv = __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])]);
+                    best = dmin(best, __dadd_rn(AR[cq + 1], cv));
+                }
+                c1 = best;
+            }
+            AR[c + 1] = finish(p, s, t, m, c1);
+        }
+        return;
+    }
+
+    // off-diagonal sub-tile: left s' in (s, ea], right s' in [t0, t]
+    const bool fAL = (delta == 0);  // left A: diagonal sub-tile of this tile (Delta = 0) or tile (I,I)
+    const bool fCR = (delta == 0);  // right C: diagonal sub-tile (gamma,gamma) (Delta = 0) or tile (J,J)
+    const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
+    AR[0] = __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]);
+    double AL[SB];  // AL[k] = A(s, s + k) for the left splits s' = s + k + 1 <= ea
+#pragma unroll
+    for (int k = 0; k < SB - 1; k++)
+        if (s + k + 1 <= ea) AL[k] = ld(&p.A[a_index(s, s + k) * pitch + m], fAL);
+#pragma unroll
+    for (int c = 0; c < SB; c++) {
+        const int t = t0 + c;
+        if (t > n) break;
+        double c1 = INFINITY;
+        if (m >= m_null(p, s, t)) {
+            double best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
+#pragma unroll
+            for (int k = 0; k < SB - 1; k++) {  // left: C of the rows below in this sub-tile (this Delta)
+                const int sp = s + k + 1;
+                if (sp > ea) break;
+                const double cv = __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])]);
+                best = dmin(best, __dadd_rn(AL[k], cv));
+            }
+#pragma unroll
+            for (int cq = 0; cq < SB; cq++) {  // right: s' = t0 + cq <= t
+                if (cq > c) break;
+                const int sp = t0 + cq;
+                const double cv = ld(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])], fCR);
+                best = dmin(best, __dadd_rn(AR[cq], cv));
+            }
+            c1 = best;
+        }
+        AR[c + 1] = finish(p, s, t, m, c1);
+    }
+}
+
+// Launch the dependent phase of tile diagonal delta; returns the launch count.
+inline int launch_dependent(const Problem &p, int delta, cudaStream_t st) {
+    const int n = p.n;
+    const int nb = (n + TB - 1) / TB;
+    const int ntiles = nb - delta;
+    const int n_mg = (p.S + 1 + 31) / 32;
+    const int phases = delta == 0 ? NSB : 2 * NSB - 1;
+    int launches = 0;
+    for (int e = 0; e < phases; e++) {
+        const int cnt = sub_count(delta, e);
+        const int warps = ntiles * cnt * n_mg;
+        const int blocks = (warps * 32 + DEP_THREADS - 1) / DEP_THREADS;
+        bool has_product;
+        if (delta == 0) {
+            has_product = e >= 2;
+        } else {
+            int a, g;
+            sub_at(delta, e, 0, a, g);
+            has_product = !(cnt == 1 && a == NSB - 1 && g == 0);
+        }
+        if (has_product) {
+            k_sub_product<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e);
+            launches++;
+        }
+        for (int r = SB - 1; r >= 0; r--) {
+            k_sub_leaf<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, r);
+            launches++;
+        }
+    }
+    return launches;
+}

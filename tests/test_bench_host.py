@@ -1,0 +1,51 @@
+"""Host-side pieces of bench.py (no GPU): the reference arm's JSON line and the
+algorithmic-bytes model of the wavefront roofline."""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import bench  # noqa: E402
+
+
+def test_transitions_formula():
+    # nominal transitions: every cell of diagonal d has d F_ck candidates + 1 F_all candidate
+    L, S = 7, 11
+    n = L + 1
+    brute = sum((d + 1) * (S + 1) for d in range(1, L + 1) for s in range(1, n - d + 1))
+    assert bench.n_transitions(L, S) == brute
+
+
+def test_alg_bytes_wavefront_bruteforce():
+    """Distinct rows read per diagonal, by enumerating the cells each candidate touches."""
+    L, S = 9, 3
+    n = L + 1
+    rows = 0
+    for d in range(1, L + 1):
+        touched = set()
+        for s in range(1, n - d + 1):
+            t = s + d
+            for k in range(1, d + 1):
+                touched.add((s, s + k - 1))  # prefix row C[s, s'-1]
+                touched.add((s + k, t))  # suffix row C[s', t]
+            touched.add((s + 1, t))  # F_all row (also a suffix row)
+        rows += len(touched)
+    cells = n * (n + 1) // 2
+    assert bench.alg_bytes_wavefront(L, S) == 8.0 * (S + 1) * (rows + cells)
+
+
+def test_reference_arm_json_line():
+    env = dict(os.environ, ROTOR_REF_WINDOW="30")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "0"], capture_output=True, text=True, env=env, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference"
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "cpu_baseline",
+              "e2e", "config"):
+        assert k in line
+    assert line["value"] > 0 and line["cpu_baseline"]["kind"] == "oracle"
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
