@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(DEP_THREADS) k_sub_product(Problem p, int delt
         partial = delta >= 2;
     }
     if (hi1 < lo1 && hi2 < lo2) return;
-    if (m > S) return;
+    if (m > S || s0 > n || t0 > n) return;  // sub-tiles past the last stage have no cells
     const int64_t pitch = p.pitch;
     double acc[SB][SB];
 #pragma unroll
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(DEP_THREADS) k_sub_leaf(Problem p, int delta, 
     const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
     const int s = s0 + r;
     const int ea = s0 + SB - 1;  // last row of this row sub-block
-    if (s > n || m > S) return;
+    if (s > n || t0 > n || m > S) return;  // sub-tiles past the last stage have no cells
     const int64_t pitch = p.pitch;
     double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
 
