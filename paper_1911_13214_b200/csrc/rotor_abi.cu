@@ -123,6 +123,7 @@ rotor::Problem make_problem(const Layout &y, char *ws, const rotor_options &o) {
     p.C = (double *)(ws + y.off_C) + rotor::kPad;  // column m = 0 of row 0
     p.D = y.has_D ? (uint16_t *)(ws + y.off_D) + rotor::kPad : nullptr;
     p.A = y.has_A ? (double *)(ws + y.off_A) + rotor::kPad : nullptr;
+    p.flags = y.has_A ? (int *)(ws + y.off_tiled) : nullptr;
     p.res_cost = (double *)(ws + y.off_res);
     p.res_nops = (int64_t *)(ws + y.off_res + 8);
     p.res_status = (int32_t *)(ws + y.off_res + 16);

@@ -35,7 +35,8 @@ struct Problem {
     int32_t *mnullT;
     double *C;
     uint16_t *D;  // nullable
-    double *A;    // nullable: A(s,c,m) = fl(fl(P[c]-P[s-1]) + C(s,c,m)), same layout as C (tiled fill)
+    double *A;    // nullable: A(s,c,m) = fl(fl(P[c]-P[s-1]) + C(s,c,m)), row a_index(s,c) (tiled fill)
+    int *flags;   // nullable: tiled fill's leaf look-back flags (tiled_extra_bytes)
     // reconstruction / results
     int4 *stack;
     int32_t stack_cap;

@@ -222,7 +222,8 @@ bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t pitch,
 
 }  // namespace tiled
 
-size_t tiled_extra_bytes(int, int) { return 0; }  // the A table is part of the Layout (rotor_abi.cu)
+// Scratch of the tiled fill beyond the A table (which is part of the Layout): the leaf flags.
+size_t tiled_extra_bytes(int L, int S) { return tiled::leaf_flag_bytes(L, S); }
 
 // Returns the number of kernels launched, or -1 on a launch/setup error.
 int launch_fill_tiled(const Problem &p, cudaStream_t st) {
@@ -241,14 +242,15 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
     if (!make_map(&tmA, p.A - kPad, rows + kPadRows, p.pitch, TM, TB) ||
         !make_map(&tmC, p.C - kPad, rows + kPadRows, p.pitch, TMB, TB))
         return -1;
-    int launches = 0;
+    if (!p.flags || cudaMemsetAsync(p.flags, 0, leaf_flag_bytes(p.L, p.S), st) != cudaSuccess) return -1;
+    int launches = 0, phase_id = 0;
     for (int delta = 0; delta < nb; delta++) {
         if (delta >= 2) {
             dim3 grid((p.S + 1 + TM - 1) / TM, nb - delta);
             k_tile_middle<<<grid, THREADS, SMEM_BYTES, st>>>(tmA, tmC, p, delta);
             launches++;
         }
-        launches += launch_dependent(p, delta, st);
+        launches += launch_dependent(p, delta, st, p.flags, phase_id);
     }
     return launches;
 }

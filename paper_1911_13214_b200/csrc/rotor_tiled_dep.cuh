@@ -135,26 +135,18 @@ __device__ __forceinline__ double finish(const Problem &p, int s, int t, int m, 
     return a;
 }
 
-// Leaf: local row r of every sub-tile of phase e.  The lane walks the row's
-// SB cells left to right; right-range A operands of the row stay in registers.
-__global__ void __launch_bounds__(DEP_THREADS) k_sub_leaf(Problem p, int delta, int e, int r) {
-    const int n = p.n, S = p.S;
-    const int nb = (n + TB - 1) / TB;
-    const int ntiles = nb - delta;
-    const int cnt = sub_count(delta, e);
-    const int n_mg = (S + 1 + 31) / 32;
-    const int item = (blockIdx.x * DEP_THREADS + threadIdx.x) >> 5;
-    if (item >= ntiles * cnt * n_mg) return;
-    const int m = (item % n_mg) * 32 + (threadIdx.x & 31);
-    const int rest = item / n_mg;
-    int alpha, gamma;
-    sub_at(delta, e, rest % cnt, alpha, gamma);
-    const int I = rest / cnt, J = I + delta;
+// One local row r of sub-tile (alpha, gamma) of tile I, at one m.  The lane
+// walks the row's SB cells left to right; right-range A operands stay in
+// registers.
+__device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int alpha, int gamma, int I, int r,
+                                         int m) {
+    const int n = p.n;
+    const int J = I + delta;
     const int i0 = I * TB + 1, j0 = J * TB + 1;
     const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
     const int s = s0 + r;
     const int ea = s0 + SB - 1;  // last row of this row sub-block
-    if (s > n || t0 > n || m > S) return;  // sub-tiles past the last stage have no cells
+    if (s > n || t0 > n || m > p.S) return;  // sub-tiles past the last stage have no cells
     const int64_t pitch = p.pitch;
     double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
 
@@ -221,12 +213,63 @@ __global__ void __launch_bounds__(DEP_THREADS) k_sub_leaf(Problem p, int delta, 
     }
 }
 
+// Leaf phase e: CTA = one sub-tile x LEAF_M consecutive m (thread = one m),
+// all SB local rows bottom-up in ONE launch.  Row r at m reads rows > r at
+// m - shift, which may belong to lower m-chunks (other CTAs): after each row a
+// CTA publishes `flags[sub][chunk] = (phase_id << 4) | rows_done` (release) and
+// before each row waits (acquire) until every lower chunk of the same sub-tile
+// has done the rows below.  CTAs of lower chunks have lower blockIdx and never
+// wait on higher ones, so the chain always progresses (decoupled look-back).
+constexpr int LEAF_M = 128;
+
+__global__ void __launch_bounds__(LEAF_M) k_sub_leaf(Problem p, int delta, int e, int *flags, int phase_id) {
+    const int n = p.n;
+    const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
+    const int cnt = sub_count(delta, e);
+    const int q = blockIdx.x % n_chunks;
+    const int sub = blockIdx.x / n_chunks;  // tile I * cnt + sub-tile index
+    int alpha, gamma;
+    sub_at(delta, e, sub % cnt, alpha, gamma);
+    const int I = sub / cnt;
+    const int m = q * LEAF_M + threadIdx.x;
+    int *my_flags = flags + (int64_t)sub * n_chunks;
+    (void)n;
+    for (int r = SB - 1; r >= 0; r--) {
+        if (r < SB - 1) {
+            const int need = (phase_id << 4) | (SB - 1 - r);  // rows SB-1 .. r+1 done
+            for (int qq = threadIdx.x; qq < q; qq += LEAF_M) {
+                int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(my_flags + qq) : "memory");
+                } while (v < need);
+            }
+            __syncthreads();
+        }
+        leaf_row(p, delta, e, alpha, gamma, I, r, m);
+        __syncthreads();  // every thread of this chunk finished row r
+        if (threadIdx.x == 0) {
+            __threadfence();
+            const int done = (phase_id << 4) | (SB - r);
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(my_flags + q), "r"(done) : "memory");
+        }
+    }
+}
+
+// Flags of the leaf look-back: one int per (sub-tile of a phase, m-chunk).
+inline size_t leaf_flag_bytes(int L, int S) {
+    const int nb = (L + 1 + TB - 1) / TB;
+    return (size_t)nb * NSB * ((S + 1 + LEAF_M - 1) / LEAF_M) * sizeof(int);
+}
+
 // Launch the dependent phase of tile diagonal delta; returns the launch count.
-inline int launch_dependent(const Problem &p, int delta, cudaStream_t st) {
+// phase_id: running counter of leaf launches in this solve (flags zeroed at
+// the start of the fill, so phase ids >= 1 never match stale values).
+inline int launch_dependent(const Problem &p, int delta, cudaStream_t st, int *flags, int &phase_id) {
     const int n = p.n;
     const int nb = (n + TB - 1) / TB;
     const int ntiles = nb - delta;
     const int n_mg = (p.S + 1 + 31) / 32;
+    const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int phases = delta == 0 ? NSB : 2 * NSB - 1;
     int launches = 0;
     for (int e = 0; e < phases; e++) {
@@ -245,10 +288,8 @@ inline int launch_dependent(const Problem &p, int delta, cudaStream_t st) {
             k_sub_product<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e);
             launches++;
         }
-        for (int r = SB - 1; r >= 0; r--) {
-            k_sub_leaf<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, r);
-            launches++;
-        }
+        k_sub_leaf<<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
+        launches++;
     }
     return launches;
 }
