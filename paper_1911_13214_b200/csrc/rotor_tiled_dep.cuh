@@ -45,16 +45,23 @@ __host__ __device__ inline void sub_at(int delta, int e, int q, int &alpha, int 
 // otherwise written by an earlier tile diagonal -> plain (L1-cacheable).
 __device__ __forceinline__ double ld(const double *p, bool fresh) { return fresh ? __ldcg(p) : *p; }
 
-// Product for one sub-tile, one m (lane), an SB x SB register tile.
-__global__ void __launch_bounds__(DEP_THREADS) k_sub_product(Problem p, int delta, int e) {
+// Product for one sub-tile: a warp covers 16 consecutive m; lane = (m, half),
+// each lane an SB x (SB/2) register tile (columns half*4 .. half*4+3), so the
+// kernel fits ~100 registers (occupancy for the load latency); the operand
+// loads of split k+1 are issued before the arithmetic of split k.
+constexpr int PH = SB / 2;  // columns per lane
+
+__global__ void __launch_bounds__(DEP_THREADS, 3) k_sub_product(Problem p, int delta, int e) {
     const int n = p.n, S = p.S;
     const int nb = (n + TB - 1) / TB;
     const int ntiles = nb - delta;
     const int cnt = sub_count(delta, e);
-    const int n_mg = (S + 1 + 31) / 32;
+    const int n_mg = (S + 1 + 15) / 16;
     const int item = (blockIdx.x * DEP_THREADS + threadIdx.x) >> 5;
     if (item >= ntiles * cnt * n_mg) return;
-    const int m = (item % n_mg) * 32 + (threadIdx.x & 31);
+    const int lane = threadIdx.x & 31;
+    const int m = (item % n_mg) * 16 + (lane & 15);
+    const int jh = (lane >> 4) * PH;  // first column of this lane
     const int rest = item / n_mg;
     int alpha, gamma;
     sub_at(delta, e, rest % cnt, alpha, gamma);
@@ -83,38 +90,50 @@ __global__ void __launch_bounds__(DEP_THREADS) k_sub_product(Problem p, int delt
     if (hi1 < lo1 && hi2 < lo2) return;
     if (m > S || s0 > n || t0 > n) return;  // sub-tiles past the last stage have no cells
     const int64_t pitch = p.pitch;
-    double acc[SB][SB];
+    const int tl = t0 + jh;  // first column of this lane
+    double acc[SB][PH];
 #pragma unroll
     for (int i = 0; i < SB; i++)
 #pragma unroll
-        for (int j = 0; j < SB; j++) {
-            const int s = s0 + i, t = t0 + j;
+        for (int j = 0; j < PH; j++) {
+            const int s = s0 + i, t = tl + j;
             acc[i][j] = (partial && s <= n && t <= n) ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
         }
     for (int r = 0; r < 2; r++) {
         const int lo = r ? lo2 : lo1, hi = r ? hi2 : hi1;
         const bool fA = r ? fA2 : fA1, fC = r ? fC2 : fC1;
-        for (int sp = lo; sp <= hi; sp++) {
-            const int w = p.wx[sp - 1];
-            if (m < w) continue;  // every cell this candidate feeds is gated (m < w <= m_null)
-            const double *ap = p.A + a_index(s0, sp - 1) * pitch + m;  // A(s0+i, sp-1): consecutive rows
-            const double *cp = p.C + cell_index(n, sp, t0) * pitch + (m - w);  // C(sp, t0+j): consecutive rows
-            double a[SB], c[SB];
+        if (hi < lo) continue;
+        // two splits per iteration: all their operand loads are issued before the
+        // arithmetic.  A skipped split (m < w: every cell it feeds is gated,
+        // m < w <= m_null) contributes +inf.
+        for (int sp = lo; sp <= hi; sp += 2) {
+            double a[2][SB], c[2][PH];
 #pragma unroll
-            for (int i = 0; i < SB; i++) a[i] = (s0 + i <= n) ? ld(ap + i * pitch, fA) : INFINITY;
+            for (int u = 0; u < 2; u++) {
+                const int q = sp + u;
+                const int w = q <= hi ? p.wx[q - 1] : 0;
+                const bool use = q <= hi && m >= w;
+                const double *ap = p.A + a_index(s0, q - 1) * pitch + m;           // A(s0+i, q-1)
+                const double *cp = p.C + cell_index(n, q, tl) * pitch + (m - w);  // C(q, tl+j)
 #pragma unroll
-            for (int j = 0; j < SB; j++) c[j] = (t0 + j <= n) ? ld(cp + j * pitch, fC) : INFINITY;
+                for (int i = 0; i < SB; i++) a[u][i] = (use && s0 + i <= n) ? ld(ap + i * pitch, fA) : INFINITY;
 #pragma unroll
-            for (int i = 0; i < SB; i++)
+                for (int j = 0; j < PH; j++) c[u][j] = (use && tl + j <= n) ? ld(cp + j * pitch, fC) : INFINITY;
+            }
 #pragma unroll
-                for (int j = 0; j < SB; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], c[j]));
+            for (int u = 0; u < 2; u++)
+#pragma unroll
+                for (int i = 0; i < SB; i++)
+#pragma unroll
+                    for (int j = 0; j < PH; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[u][i], c[u][j]));
         }
     }
+    if (m > S) return;
 #pragma unroll
     for (int i = 0; i < SB; i++)
 #pragma unroll
-        for (int j = 0; j < SB; j++) {
-            const int s = s0 + i, t = t0 + j;
+        for (int j = 0; j < PH; j++) {
+            const int s = s0 + i, t = tl + j;
             if (s <= n && t <= n) p.C[cell_index(n, s, t) * pitch + m] = acc[i][j];
         }
 }
@@ -138,6 +157,7 @@ __device__ __forceinline__ double finish(const Problem &p, int s, int t, int m, 
 // One local row r of sub-tile (alpha, gamma) of tile I, at one m.  The lane
 // walks the row's SB cells left to right; right-range A operands stay in
 // registers.
+template <bool DIAG>
 __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int alpha, int gamma, int I, int r,
                                          int m) {
     const int n = p.n;
@@ -150,7 +170,7 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
     const int64_t pitch = p.pitch;
     double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
 
-    if (delta == 0 && e == 0) {  // diagonal sub-tile: cells (s, s+1..ea), splits s' in (s, t]
+    if (DIAG) {  // diagonal sub-tile (delta = 0, e = 0): cells (s, s+1..ea), splits s' in (s, t]
         const double leaf = p.A[a_index(s, s) * pitch + m];  // the leaf (k_leaf, an earlier launch)
 #pragma unroll
         for (int c = 0; c < SB; c++)  // AR[r + 1] = leaf, with compile-time register indices
@@ -222,7 +242,8 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
 // wait on higher ones, so the chain always progresses (decoupled look-back).
 constexpr int LEAF_M = 128;
 
-__global__ void __launch_bounds__(LEAF_M) k_sub_leaf(Problem p, int delta, int e, int *flags, int phase_id) {
+template <bool DIAG>
+__global__ void __launch_bounds__(LEAF_M, 4) k_sub_leaf(Problem p, int delta, int e, int *flags, int phase_id) {
     const int n = p.n;
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int cnt = sub_count(delta, e);
@@ -245,7 +266,7 @@ __global__ void __launch_bounds__(LEAF_M) k_sub_leaf(Problem p, int delta, int e
             }
             __syncthreads();
         }
-        leaf_row(p, delta, e, alpha, gamma, I, r, m);
+        leaf_row<DIAG>(p, delta, e, alpha, gamma, I, r, m);
         __syncthreads();  // every thread of this chunk finished row r
         if (threadIdx.x == 0) {
             __threadfence();
@@ -268,7 +289,7 @@ inline int launch_dependent(const Problem &p, int delta, cudaStream_t st, int *f
     const int n = p.n;
     const int nb = (n + TB - 1) / TB;
     const int ntiles = nb - delta;
-    const int n_mg = (p.S + 1 + 31) / 32;
+    const int n_mg = (p.S + 1 + 15) / 16;  // product: a warp per (sub-tile, 16 m)
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int phases = delta == 0 ? NSB : 2 * NSB - 1;
     int launches = 0;
@@ -288,7 +309,10 @@ inline int launch_dependent(const Problem &p, int delta, cudaStream_t st, int *f
             k_sub_product<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e);
             launches++;
         }
-        k_sub_leaf<<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
+        if (delta == 0 && e == 0)
+            k_sub_leaf<true><<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
+        else
+            k_sub_leaf<false><<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
         launches++;
     }
     return launches;

@@ -35,9 +35,9 @@ __global__ void __launch_bounds__(256) kern(double *out, int iters) {
 #pragma unroll
                 for (int j = 0; j < RT; j++) {
                     double v = __dadd_rn(a[i], b[j]);
-                    if (MODE == 0) {
+                    if (MODE == 0 || (MODE == 3 && j < RT - 2)) {
                         acc[i][j] = v < acc[i][j] ? v : acc[i][j];
-                    } else if (MODE == 1) {
+                    } else if (MODE == 1 || MODE == 3) {
                         long long x = __double_as_longlong(v), y = __double_as_longlong(acc[i][j]);
                         acc[i][j] = __longlong_as_double(x < y ? x : y);
                     } else {
@@ -83,6 +83,8 @@ int main() {
     run<0, 4, 4>("dsetp-min");
     run<0, 4, 8>("dsetp-min");
     run<0, 8, 8>("dsetp-min");
+    run<3, 8, 8>("mixed (2 of 8 cols int64)");
+    run<3, 4, 8>("mixed (2 of 8 cols int64)");
     run<1, 4, 8>("int64-min");
     run<1, 8, 8>("int64-min");
     run<2, 4, 8>("dadd-only");
