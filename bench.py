@@ -394,14 +394,17 @@ def run_ours(args):
     fill_avg_ms = sum(fill_ms) / len(fill_ms)
     if kernel in ("auto", "tiled"):
         # Tiled fill: bound by the fp64 pipe: every transition is one
-        # DADD + one DSETP (+2 FSEL on the ALU pipe); B200 issues 64 fp64 lanes/clk/SM.
+        # DADD (64 lanes/clk/SM on B200) + one DSETP (half rate, 32 lanes/clk/SM), both
+        # on the fp64 pipe -> 1/64 + 1/32 clk per transition per lane-slot = 21.33
+        # transitions/clk/SM (the 2 FSEL go to the ALU pipe).
         clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        peak = 148 * 64 * clk_mhz * 1e6 / 2 / 1e9  # Gtransitions/s
+        peak = 148 * (64.0 / 3.0) * clk_mhz * 1e6 / 1e9  # Gtransitions/s
         achieved = tr / (fill_avg_ms / 1e3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gtransitions/s",
                     "frac": achieved / peak, "traffic": ncu_traffic("k_tile_middle"),
                     "kernel": "tiled fill (k_tile_middle + k_tile_dep, all tile diagonals)",
-                    "peak_model": "148 SMs x 64 fp64 lanes/clk x sm_max_mhz / 2 fp64 ops per transition",
+                    "peak_model": "148 SMs x sm_max_mhz x 21.33 transitions/clk/SM (fp64 pipe: DADD 64 "
+                                  "lanes/clk + DSETP 32 lanes/clk per SM, measured scripts/microbench_minplus.cu)",
                     "launches_per_step": fill_launches, "fill_ms_per_step": fill_avg_ms,
                     "hbm_wavefront_equiv_frac": alg_bytes_wavefront(L, S) / (fill_avg_ms / 1e3) / 1e9
                     / float(peaks["hbm_gbs"])}

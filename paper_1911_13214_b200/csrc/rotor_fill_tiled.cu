@@ -86,13 +86,14 @@ __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : 
 
 // The same exact min on the integer pipe: non-negative doubles (every
 // candidate, Q13) order like their int64 bit patterns.  DSETP runs at half the
-// DADD rate, so taking 1/4 of the mins through ISETP/SEL balances the fp64 and
-// ALU pipes.  (Pad garbage only ever reaches gated cells.)
+// DADD rate, so routing a share of the mins through ISETP/SEL looked like a way
+// to balance the fp64 and ALU pipes — measured slower on B200 (mixed 17.0 vs
+// 18.3 transitions/clk/SM, scripts/microbench_minplus.cu), so it is off.
 __device__ __forceinline__ double imin(double a, double b) {
     const long long x = __double_as_longlong(a), y = __double_as_longlong(b);
     return __longlong_as_double(y < x ? y : x);
 }
-constexpr int INT_MIN_COLS = 2;  // register-tile columns j >= RT - INT_MIN_COLS use imin
+constexpr int INT_MIN_COLS = 0;  // register-tile columns j >= RT - INT_MIN_COLS use imin
 
 // ---------------------------------------------------------------------------
 // Middle phase of tile diagonal delta >= 2: partial(s,t,m) = min over s' in
