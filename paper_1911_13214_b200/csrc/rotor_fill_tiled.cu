@@ -244,7 +244,9 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(k_tile_middle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) !=
-            cudaSuccess)
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_sub_leaf_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LEAF_SMEM) !=
+                cudaSuccess)
             return -1;
         attr = true;
     }

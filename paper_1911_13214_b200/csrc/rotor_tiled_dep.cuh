@@ -276,6 +276,120 @@ __global__ void __launch_bounds__(LEAF_M, 4) k_sub_leaf(Problem p, int delta, in
     }
 }
 
+__device__ __forceinline__ void leaf_wait(const int *my_flags, int q, int need) {
+    for (int qq = threadIdx.x; qq < q; qq += LEAF_M) {
+        int v;
+        do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(my_flags + qq) : "memory");
+        } while (v < need);
+    }
+}
+
+__device__ __forceinline__ void leaf_publish(int *flag, int value) {
+    if (threadIdx.x == 0) {
+        __threadfence();
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
+    }
+}
+
+// Off-diagonal leaf with its operands in shared memory:
+//   RS_[pair][x]   right-range C(s', t, m0+x - wx[s'-1]), s' <= t in the column
+//                  sub-block (36 pairs): the same for all 8 rows, staged once;
+//   CS_[r][c][x]   this CTA's own results C(s0+r, t0+c, m0+x), read by the
+//                  rows above at m - shift >= m0 (lower m: another chunk ->
+//                  global, behind the look-back flags).
+constexpr int NPAIR = SB * (SB + 1) / 2;
+constexpr size_t LEAF_SMEM = (size_t)(NPAIR + SB * SB) * LEAF_M * 8;
+
+__global__ void __launch_bounds__(LEAF_M) k_sub_leaf_smem(Problem p, int delta, int e, int *flags, int phase_id) {
+    extern __shared__ double lsm[];
+    double *RS_ = lsm;                   // [NPAIR][LEAF_M]
+    double *CS_ = lsm + NPAIR * LEAF_M;  // [SB][SB][LEAF_M]
+    const int n = p.n, S = p.S;
+    const int64_t pitch = p.pitch;
+    const int n_chunks = (S + 1 + LEAF_M - 1) / LEAF_M;
+    const int cnt = sub_count(delta, e);
+    const int q = blockIdx.x % n_chunks;
+    const int sub = blockIdx.x / n_chunks;
+    int alpha, gamma;
+    sub_at(delta, e, sub % cnt, alpha, gamma);
+    const int I = sub / cnt, J = I + delta;
+    const int i0 = I * TB + 1, j0 = J * TB + 1;
+    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
+    const int ea = s0 + SB - 1;
+    const int m0 = q * LEAF_M, tid = threadIdx.x, m = m0 + tid;
+    int *my_flags = flags + (int64_t)sub * n_chunks;
+    const bool live = s0 <= n && t0 <= n && m <= S;
+    const bool fresh = (delta == 0);  // right C and left A belong to this tile diagonal when delta = 0
+    const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
+
+    // stage the right-range operands (written by earlier launches): 36 independent loads
+    if (live) {
+#pragma unroll
+        for (int c = 0; c < SB; c++) {
+#pragma unroll
+            for (int cq = 0; cq <= c; cq++) {
+                const int t = t0 + c, sp = t0 + cq;
+                const int w = p.wx[sp - 1];
+                RS_[(c * (c + 1) / 2 + cq) * LEAF_M + tid] =
+                    (t <= n && m >= w) ? ld(&p.C[cell_index(n, sp, t) * pitch + (m - w)], fresh) : INFINITY;
+            }
+        }
+    }
+    for (int r = SB - 1; r >= 0; r--) {
+        if (r < SB - 1) leaf_wait(my_flags, q, (phase_id << 4) | (SB - 1 - r));
+        __syncthreads();  // rows below: other chunks (flags) and this chunk (CS_) complete
+        const int s = s0 + r;
+        if (live && s <= n) {
+            double AL[SB - 1], part[SB], AR[SB + 1];
+#pragma unroll
+            for (int k = 0; k < SB - 1; k++)
+                AL[k] = (s + k + 1 <= ea) ? ld(&p.A[a_index(s, s + k) * pitch + m], fresh) : INFINITY;
+#pragma unroll
+            for (int c = 0; c < SB; c++)
+                part[c] = (partial && t0 + c <= n) ? __ldcg(&p.C[cell_index(n, s, t0 + c) * pitch + m]) : INFINITY;
+            AR[0] = __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]);
+#pragma unroll
+            for (int c = 0; c < SB; c++) {
+                const int t = t0 + c;
+                if (t > n) break;
+                double c1 = INFINITY;
+                if (m >= m_null(p, s, t)) {  // every shifted index below is >= 0 (DESIGN Q6)
+                    double best = part[c];
+#pragma unroll
+                    for (int k = 0; k < SB - 1; k++) {  // left: rows below in this sub-tile
+                        const int sp = s + k + 1;
+                        if (sp > ea) break;
+                        const int mm = m - p.wx[sp - 1];
+                        const double cv = (mm >= m0) ? CS_[((sp - s0) * SB + c) * LEAF_M + (mm - m0)]
+                                                     : __ldcg(&p.C[cell_index(n, sp, t) * pitch + mm]);
+                        best = dmin(best, __dadd_rn(AL[k], cv));
+                    }
+#pragma unroll
+                    for (int cq = 0; cq <= c; cq++)  // right: staged column sub-block
+                        best = dmin(best, __dadd_rn(AR[cq], RS_[(c * (c + 1) / 2 + cq) * LEAF_M + tid]));
+                    c1 = best;
+                }
+                double cc = c1;
+                if (!p.restricted && m >= m_all(p, s, t)) {  // F_all: row s+1 at m - wbx[s] >= 0
+                    const int mm = m - p.wbx[s];
+                    const double sub_v = (s + 1 <= ea && mm >= m0)
+                                             ? CS_[((s + 1 - s0) * SB + c) * LEAF_M + (mm - m0)]
+                                             : __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + mm]);
+                    cc = dmin(cc, __dadd_rn(p.w[s], sub_v));
+                }
+                p.C[cell_index(n, s, t) * pitch + m] = cc;
+                CS_[(r * SB + c) * LEAF_M + tid] = cc;
+                const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), cc);
+                if (t < n) p.A[a_index(s, t) * pitch + m] = a;
+                AR[c + 1] = a;
+            }
+        }
+        __syncthreads();  // row r of this chunk complete (global and CS_)
+        leaf_publish(my_flags + q, (phase_id << 4) | (SB - r));
+    }
+}
+
 // Flags of the leaf look-back: one int per (sub-tile of a phase, m-chunk).
 inline size_t leaf_flag_bytes(int L, int S) {
     const int nb = (L + 1 + TB - 1) / TB;
@@ -312,7 +426,7 @@ inline int launch_dependent(const Problem &p, int delta, cudaStream_t st, int *f
         if (delta == 0 && e == 0)
             k_sub_leaf<true><<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
         else
-            k_sub_leaf<false><<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
+            k_sub_leaf_smem<<<ntiles * cnt * n_chunks, LEAF_M, LEAF_SMEM, st>>>(p, delta, e, flags, ++phase_id);
         launches++;
     }
     return launches;
