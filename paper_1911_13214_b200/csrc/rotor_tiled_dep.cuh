@@ -206,13 +206,17 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
 #pragma unroll
     for (int k = 0; k < SB - 1; k++)
         if (s + k + 1 <= ea) AL[k] = ld(&p.A[a_index(s, s + k) * pitch + m], fAL);
+    // pass 1 — independent across the row's cells (all loads in flight together):
+    // the partial, the left range (rows below), and the F_all operand.
+    double B[SB], F[SB];
+    bool gate[SB];
 #pragma unroll
     for (int c = 0; c < SB; c++) {
         const int t = t0 + c;
-        if (t > n) break;
-        double c1 = INFINITY;
-        if (m >= m_null(p, s, t)) {
-            double best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
+        gate[c] = t <= n && m >= m_null(p, s, t);  // every shifted index is >= 0 under it (DESIGN Q6)
+        double best = INFINITY;
+        if (gate[c]) {
+            best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
 #pragma unroll
             for (int k = 0; k < SB - 1; k++) {  // left: C of the rows below in this sub-tile (this Delta)
                 const int sp = s + k + 1;
@@ -220,6 +224,20 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
                 const double cv = __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])]);
                 best = dmin(best, __dadd_rn(AL[k], cv));
             }
+        }
+        B[c] = best;
+        F[c] = (t <= n && !p.restricted && m >= m_all(p, s, t))  // row s+1 at m - wbx[s] >= 0, final
+                   ? __dadd_rn(p.w[s], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - p.wbx[s])]))
+                   : INFINITY;
+    }
+    // pass 2 — the chain along the row: right range with the row's own A operands
+#pragma unroll
+    for (int c = 0; c < SB; c++) {
+        const int t = t0 + c;
+        if (t > n) break;
+        double c1 = INFINITY;
+        if (gate[c]) {
+            double best = B[c];
 #pragma unroll
             for (int cq = 0; cq < SB; cq++) {  // right: s' = t0 + cq <= t
                 if (cq > c) break;
@@ -229,7 +247,11 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
             }
             c1 = best;
         }
-        AR[c + 1] = finish(p, s, t, m, c1);
+        const double cc = dmin(c1, F[c]);
+        p.C[cell_index(n, s, t) * pitch + m] = cc;
+        const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), cc);
+        if (t < n) p.A[a_index(s, t) * pitch + m] = a;
+        AR[c + 1] = a;
     }
 }
 
@@ -298,6 +320,10 @@ __device__ __forceinline__ void leaf_publish(int *flag, int value) {
 //   CS_[r][c][x]   this CTA's own results C(s0+r, t0+c, m0+x), read by the
 //                  rows above at m - shift >= m0 (lower m: another chunk ->
 //                  global, behind the look-back flags).
+// Measured slower than the register leaf (147 vs 119 ms at config 4: the
+// chunk-boundary lanes fall back to serialized global loads and 102 KB of
+// shared memory leaves 8 warps/SM), so it is not launched by default.
+constexpr bool LEAF_USE_SMEM = false;
 constexpr int NPAIR = SB * (SB + 1) / 2;
 constexpr size_t LEAF_SMEM = (size_t)(NPAIR + SB * SB) * LEAF_M * 8;
 
@@ -425,8 +451,10 @@ inline int launch_dependent(const Problem &p, int delta, cudaStream_t st, int *f
         }
         if (delta == 0 && e == 0)
             k_sub_leaf<true><<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
-        else
+        else if (LEAF_USE_SMEM)
             k_sub_leaf_smem<<<ntiles * cnt * n_chunks, LEAF_M, LEAF_SMEM, st>>>(p, delta, e, flags, ++phase_id);
+        else
+            k_sub_leaf<false><<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
         launches++;
     }
     return launches;
