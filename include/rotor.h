@@ -146,6 +146,41 @@ int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_ch
                       rotor_op *ops, const int64_t *ops_offsets, const int64_t *ops_caps, int64_t *n_ops,
                       int32_t *status);
 
+/* ---------------------------------------------------------------------------
+ * Sharded single-table solve, for one process per GPU.
+ * The tiled fill cuts the (s,t) triangle into 32x32-stage tiles processed by
+ * tile diagonal delta = 0 .. rotor_tile_blocks(L)-1; every tile of one delta
+ * depends only on tiles of smaller delta (Theorem 1 reads strictly shorter
+ * intervals).  Each rank keeps a full workspace; per delta it
+ * computes its share of the tiles (rotor_sharded_step), packs them
+ * (rotor_sharded_pack), the caller all-gathers the packed buffers (NCCL), and
+ * every rank unpacks the other ranks' tiles (rotor_sharded_pack, unpack = 1).
+ * All calls enqueue on `stream` and return immediately.  A handle owns the
+ * state of one sharded solve (several handles may coexist, e.g. to emulate
+ * ranks on one GPU).  The result equals rotor_solve's bit for bit (the same
+ * kernels compute every tile).
+ * ------------------------------------------------------------------------- */
+typedef struct rotor_shard rotor_shard;
+int32_t rotor_tile_blocks(int32_t L);                 /* ceil((L+1)/32) */
+int rotor_tile_bytes(int32_t slots, uint64_t *bytes); /* packed bytes per tile (C and A rows, all m) */
+/* discretise + limits + leaf diagonal + setup; d_chain and the workspace as in
+ * rotor_solve_device (options: kernel forced to TILED).  *out: new handle. */
+int rotor_sharded_begin(const rotor_chain *d_chain, int32_t L, uint64_t mem_limit, int32_t slots,
+                        const rotor_options *opt, void *d_workspace, uint64_t workspace_bytes, void *stream,
+                        rotor_shard **out);
+/* middle + dependent phase of the tiles I in [tile_lo, tile_hi) of diagonal delta
+ * (0 <= tile_lo <= tile_hi <= rotor_tile_blocks(L) - delta) */
+int rotor_sharded_step(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t tile_hi, void *stream);
+/* copy those tiles' C and A rows to (unpack = 0) or from (unpack = 1) d_buf:
+ * layout [tile][C|A][32 s][32 t][S+1] fp64; buf_bytes >= count * rotor_tile_bytes */
+int rotor_sharded_pack(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t tile_hi, void *d_buf,
+                       uint64_t buf_bytes, int32_t unpack, void *stream);
+/* Algorithm 2 on the completed table; outputs as in rotor_solve_device.  Also
+ * makes this table the "last solve" of the thread for rotor_export_*. */
+int rotor_sharded_finish(rotor_shard *h, void *stream, double *d_cost, rotor_op *d_ops, int64_t ops_cap,
+                         int64_t *d_n_ops, int32_t *d_status);
+int rotor_sharded_free(rotor_shard *h);
+
 /* Longest-processing-time partition of n_items weighted items over n_parts
  * parts (host helper for sharding independent solves across GPUs/ranks).
  * part_of[i] in 0..n_parts-1; deterministic (ties -> lowest part index). */

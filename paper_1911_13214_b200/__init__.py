@@ -79,6 +79,14 @@ _lib.rotor_transitions.restype = _d
 _lib.rotor_export_tables.argtypes = [_vp, _vp, _i64]
 _lib.rotor_last_timings.argtypes = [_P(rotor_timings)]
 _lib.rotor_export_rows.argtypes = [_vp, _vp, _i64, _vp]
+_lib.rotor_tile_blocks.argtypes = [_i32]
+_lib.rotor_tile_blocks.restype = _i32
+_lib.rotor_tile_bytes.argtypes = [_i32, _P(_u64)]
+_lib.rotor_sharded_begin.argtypes = [_P(rotor_chain), _i32, _u64, _i32, _P(rotor_options), _vp, _u64, _vp, _P(_vp)]
+_lib.rotor_sharded_step.argtypes = [_vp, _i32, _i32, _i32, _vp]
+_lib.rotor_sharded_pack.argtypes = [_vp, _i32, _i32, _i32, _vp, _u64, _i32, _vp]
+_lib.rotor_sharded_finish.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]
+_lib.rotor_sharded_free.argtypes = [_vp]
 _lib.rotor_release.argtypes = []
 _lib.rotor_last_error.restype = _c.c_char_p
 _lib.rotor_version.restype = _i32
@@ -89,6 +97,8 @@ EXPORTS = (
     "rotor_solve_batch", "rotor_partition_lpt", "rotor_transitions", "rotor_export_tables", "rotor_export_rows",
     "rotor_last_timings",
     "rotor_release", "rotor_last_error", "rotor_version",
+    "rotor_tile_blocks", "rotor_tile_bytes", "rotor_sharded_begin", "rotor_sharded_step", "rotor_sharded_pack",
+    "rotor_sharded_finish", "rotor_sharded_free",
 )
 
 
@@ -283,6 +293,58 @@ def partition_lpt(weights, n_parts: int) -> np.ndarray:
     out = np.zeros(len(w), dtype=np.int32)
     _check(_lib.rotor_partition_lpt(w.ctypes.data_as(_P(_d)), len(w), int(n_parts), out.ctypes.data_as(_P(_i32))))
     return out
+
+
+def tile_blocks(L: int) -> int:
+    """Number of 32-stage blocks of the tiled fill: tile diagonals are 0 .. tile_blocks(L)-1."""
+    return int(_lib.rotor_tile_blocks(int(L)))
+
+
+def tile_bytes(slots: int) -> int:
+    b = _u64()
+    _check(_lib.rotor_tile_bytes(int(slots), _c.byref(b)))
+    return int(b.value)
+
+
+class Shard:
+    """One rank's sharded single-table solve (rotor_sharded_* of include/rotor.h).
+
+    d_chain: dict of device tensors as for solve_device; workspace: device uint8
+    tensor of >= workspace_bytes(L, slots, kernel="tiled").
+    """
+
+    def __init__(self, d_chain: dict, L: int, mem_limit: int, slots: int, workspace, stream=None, **opts):
+        self.L, self.S = int(L), int(slots)
+        self._keep = (d_chain, workspace)
+        c = rotor_chain(*(int(d_chain[k].data_ptr()) for k in ("uf", "ub", "wx", "wbx", "wy", "of", "ob")))
+        o = _options(**opts)
+        ws_ptr, ws_bytes = _ws(workspace)
+        h = _vp()
+        _check(_lib.rotor_sharded_begin(_c.byref(c), self.L, int(mem_limit), self.S, _c.byref(o), ws_ptr, ws_bytes,
+                                        _stream_ptr(stream), _c.byref(h)))
+        self.h = h.value
+
+    def step(self, delta: int, lo: int, hi: int, stream=None):
+        _check(_lib.rotor_sharded_step(self.h, int(delta), int(lo), int(hi), _stream_ptr(stream)))
+
+    def pack(self, delta: int, lo: int, hi: int, buf, unpack: bool = False, stream=None):
+        nbytes = int(buf.numel() * buf.element_size())
+        _check(_lib.rotor_sharded_pack(self.h, int(delta), int(lo), int(hi), int(buf.data_ptr()), nbytes,
+                                       1 if unpack else 0, _stream_ptr(stream)))
+
+    def finish(self, out: dict, stream=None):
+        cap = int(out["ops"].shape[0])
+        _check(_lib.rotor_sharded_finish(self.h, _stream_ptr(stream), int(out["cost"].data_ptr()),
+                                         int(out["ops"].data_ptr()), cap, int(out["n_ops"].data_ptr()),
+                                         int(out["status"].data_ptr())))
+
+    def close(self):
+        if getattr(self, "h", None):
+            _lib.rotor_sharded_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
 
 
 def release():

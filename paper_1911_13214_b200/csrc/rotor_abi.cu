@@ -558,6 +558,110 @@ int rotor_export_tables(double *C_host, uint16_t *D_host, int64_t n_values) {
     return ROTOR_OK;
 }
 
+// ---- sharded single-table solve (one process per GPU; see include/rotor.h) ----
+struct rotor_shard {
+    Layout y;
+    rotor::Problem p;
+    rotor::TiledCtx ctx;
+    int device;
+    cudaStream_t stream;
+};
+
+int32_t rotor_tile_blocks(int32_t L) { return L < 1 ? 0 : rotor::tiled_nb(L + 1); }
+
+int rotor_tile_bytes(int32_t slots, uint64_t *bytes) {
+    if (slots < 1 || !bytes) return fail(ROTOR_EINPUT, "bad arguments");
+    *bytes = rotor::tiled_tile_bytes(slots);
+    return ROTOR_OK;
+}
+
+int rotor_sharded_begin(const rotor_chain *d_chain, int32_t L, uint64_t mem_limit, int32_t slots,
+                        const rotor_options *opt, void *d_workspace, uint64_t workspace_bytes, void *stream,
+                        rotor_shard **out) {
+    if (!out) return fail(ROTOR_EINPUT, "out is NULL");
+    *out = nullptr;
+    int r = check_args(L, mem_limit, slots);
+    if (r) return r;
+    if (!d_chain || !d_chain->uf || !d_chain->ub || !d_chain->wx || !d_chain->wbx || !d_chain->wy || !d_chain->of ||
+        !d_chain->ob)
+        return fail(ROTOR_EINPUT, "chain has a NULL array");
+    rotor_options o = opts_or_default(opt);
+    o.kernel = ROTOR_KERNEL_TILED;
+    o.keep_argmin = 0;
+    Layout y = make_layout(L, slots, o);
+    if (!d_workspace) return fail(ROTOR_EINPUT, "d_workspace is required");
+    if (workspace_bytes < y.total)
+        return fail(ROTOR_ENOMEM, "workspace too small: %llu < %zu", (unsigned long long)workspace_bytes, y.total);
+    cudaStream_t st = (cudaStream_t)stream;
+    rotor::Problem p = make_problem(y, (char *)d_workspace, o);
+    rotor::launch_precompute(*d_chain, mem_limit, p, st);
+    rotor::launch_leaf(p, st);
+    CK(cudaGetLastError());
+    rotor_shard *h = new rotor_shard();
+    if (rotor::tiled_prepare(p, &h->ctx, st)) {
+        delete h;
+        return fail(ROTOR_EDEVICE, "tiled setup failed");
+    }
+    h->y = y;
+    h->p = p;
+    h->stream = st;
+    CK(cudaGetDevice(&h->device));
+    *out = h;
+    return ROTOR_OK;
+}
+
+int rotor_sharded_step(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t tile_hi, void *stream) {
+    if (!h) return fail(ROTOR_EINPUT, "NULL shard handle");
+    const int nb = rotor::tiled_nb(h->p.n);
+    if (delta < 0 || delta >= nb || tile_lo < 0 || tile_hi > nb - delta || tile_lo > tile_hi)
+        return fail(ROTOR_EINPUT, "bad tile range [%d,%d) at delta %d", tile_lo, tile_hi, delta);
+    if (rotor::tiled_delta(h->p, &h->ctx, delta, tile_lo, tile_hi, (cudaStream_t)stream) < 0)
+        return fail(ROTOR_EDEVICE, "tiled step failed");
+    CK(cudaGetLastError());
+    return ROTOR_OK;
+}
+
+int rotor_sharded_pack(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t tile_hi, void *d_buf,
+                       uint64_t buf_bytes, int32_t unpack, void *stream) {
+    if (!h) return fail(ROTOR_EINPUT, "NULL shard handle");
+    const int nb = rotor::tiled_nb(h->p.n);
+    if (delta < 0 || delta >= nb || tile_lo < 0 || tile_hi > nb - delta || tile_lo > tile_hi || !d_buf)
+        return fail(ROTOR_EINPUT, "bad pack arguments");
+    if (buf_bytes < (uint64_t)(tile_hi - tile_lo) * rotor::tiled_tile_bytes(h->p.S))
+        return fail(ROTOR_ENOMEM, "pack buffer too small");
+    rotor::tiled_pack(h->p, delta, tile_lo, tile_hi, (double *)d_buf, unpack ? 1 : 0, (cudaStream_t)stream);
+    CK(cudaGetLastError());
+    return ROTOR_OK;
+}
+
+int rotor_sharded_free(rotor_shard *h) {
+    delete h;
+    return ROTOR_OK;
+}
+
+int rotor_sharded_finish(rotor_shard *h, void *stream, double *d_cost, rotor_op *d_ops, int64_t ops_cap,
+                         int64_t *d_n_ops, int32_t *d_status) {
+    if (!h) return fail(ROTOR_EINPUT, "NULL shard handle");
+    if (!d_cost || !d_n_ops || !d_status || (ops_cap > 0 && !d_ops)) return fail(ROTOR_EINPUT, "bad outputs");
+    g_last.valid = true;
+    g_last.y = h->y;
+    g_last.p = h->p;
+    g_last.device = h->device;
+    g_last.stream = (cudaStream_t)stream;
+    g_last.profiled = false;
+    rotor::Problem p = h->p;
+    // the precompute wrote its status into the workspace's result slot: carry it over
+    CK(cudaMemcpyAsync(d_status, p.res_status, 4, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
+    p.res_cost = d_cost;
+    p.res_nops = d_n_ops;
+    p.res_status = d_status;
+    p.ops = d_ops;
+    p.ops_cap = ops_cap < 0 ? 0 : ops_cap;
+    rotor::launch_reconstruct(p, (cudaStream_t)stream);
+    CK(cudaGetLastError());
+    return ROTOR_OK;
+}
+
 int rotor_export_rows(const int32_t *s, const int32_t *t, int64_t n_rows, double *C_host) {
     if (!g_last.valid) return fail(ROTOR_EINPUT, "no solve on this thread");
     if (n_rows < 0 || (n_rows > 0 && (!s || !t || !C_host))) return fail(ROTOR_EINPUT, "bad export_rows arguments");

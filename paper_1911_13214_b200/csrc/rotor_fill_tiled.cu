@@ -104,7 +104,7 @@ constexpr int INT_MIN_COLS = 0;  // register-tile columns j >= RT - INT_MIN_COLS
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC, Problem p,
-                  int delta) {
+                  int delta, int tile_lo) {
     extern __shared__ __align__(1024) double smem[];  // no static smem: the dynamic base is aligned
     double *As = smem;                     // [STAGES][KC][TB][TM]
     double *Bs = smem + STAGES * A_STAGE;  // [STAGES][KC][TB][TMB]
@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t *empty = full + STAGES;
     int *soff = reinterpret_cast<int *>(empty + STAGES);  // [STAGES][KC] column offset of each C box
 
-    const int I = blockIdx.y, J = I + delta;
+    const int I = tile_lo + blockIdx.y, J = I + delta;
     const int i0 = I * TB + 1, j0 = J * TB + 1, i1 = i0 + TB;
     const int m0 = blockIdx.x * TM;
     const int n = p.n;
@@ -238,9 +238,13 @@ bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t pitch,
 // Scratch of the tiled fill beyond the A table (which is part of the Layout): the leaf flags.
 size_t tiled_extra_bytes(int L, int S) { return tiled::leaf_flag_bytes(L, S); }
 
-// Returns the number of kernels launched, or -1 on a launch/setup error.
-int launch_fill_tiled(const Problem &p, cudaStream_t st) {
+int tiled_nb(int n) { return (n + tiled::TB - 1) / tiled::TB; }
+
+// Per-solve setup: kernel attributes, the two tensor maps (over the whole
+// allocations: left pad columns and spare rows included), zeroed leaf flags.
+int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     using namespace tiled;
+    static_assert(sizeof(CUtensorMap) <= sizeof(ctx->tmA), "tensor map storage");
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(k_tile_middle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) !=
@@ -251,23 +255,71 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
         attr = true;
     }
     const int n = p.n;
-    const int nb = (n + TB - 1) / TB;
     const int64_t rows = (int64_t)n * (n + 1) / 2;
-    CUtensorMap tmA, tmC;  // over the whole allocations: left pad columns and spare rows included
-    if (!make_map(&tmA, p.A - kPad, rows + kPadRows, p.pitch, TM, TB) ||
-        !make_map(&tmC, p.C - kPad, rows + kPadRows, p.pitch, TMB, TB))
+    if (!make_map(reinterpret_cast<CUtensorMap *>(ctx->tmA), p.A - kPad, rows + kPadRows, p.pitch, TM, TB) ||
+        !make_map(reinterpret_cast<CUtensorMap *>(ctx->tmC), p.C - kPad, rows + kPadRows, p.pitch, TMB, TB))
         return -1;
     if (!p.flags || cudaMemsetAsync(p.flags, 0, leaf_flag_bytes(p.L, p.S), st) != cudaSuccess) return -1;
-    int launches = 0, phase_id = 0;
-    for (int delta = 0; delta < nb; delta++) {
-        if (delta >= 2) {
-            dim3 grid((p.S + 1 + TM - 1) / TM, nb - delta);
-            k_tile_middle<<<grid, THREADS, SMEM_BYTES, st>>>(tmA, tmC, p, delta);
-            launches++;
-        }
-        launches += launch_dependent(p, delta, st, p.flags, phase_id);
+    ctx->phase_id = 0;
+    return 0;
+}
+
+// Middle + dependent phase of the tiles I in [tile_lo, tile_hi) of tile
+// diagonal delta.  Returns the number of kernels launched.
+int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int tile_hi, cudaStream_t st) {
+    using namespace tiled;
+    if (tile_hi <= tile_lo) return 0;
+    int launches = 0;
+    if (delta >= 2) {
+        dim3 grid((p.S + 1 + TM - 1) / TM, tile_hi - tile_lo);
+        k_tile_middle<<<grid, THREADS, SMEM_BYTES, st>>>(*reinterpret_cast<const CUtensorMap *>(ctx->tmA),
+                                                         *reinterpret_cast<const CUtensorMap *>(ctx->tmC), p,
+                                                         delta, tile_lo);
+        launches++;
     }
+    return launches + launch_dependent(p, delta, tile_lo, tile_hi, st, p.flags, ctx->phase_id);
+}
+
+// Returns the number of kernels launched, or -1 on a launch/setup error.
+int launch_fill_tiled(const Problem &p, cudaStream_t st) {
+    TiledCtx ctx;
+    if (tiled_prepare(p, &ctx, st)) return -1;
+    const int nb = tiled_nb(p.n);
+    int launches = 0;
+    for (int delta = 0; delta < nb; delta++) launches += tiled_delta(p, &ctx, delta, 0, nb - delta, st);
     return launches;
+}
+
+// ---------------------------------------------------------------------------
+// Sharded fill support: pack / unpack the C and A rows of a range of tiles of
+// one tile diagonal into a contiguous buffer [tile][C|A][TB s][TB t][S+1].
+// Cells that do not exist (s > t, t > n; A at t = n) are skipped both ways.
+// ---------------------------------------------------------------------------
+size_t tiled_tile_bytes(int S) { return (size_t)2 * tiled::TB * tiled::TB * (S + 1) * sizeof(double); }
+
+__global__ void k_tile_pack(Problem p, int delta, int tile_lo, double *buf, int unpack) {
+    using namespace tiled;
+    const int n = p.n, W = p.S + 1;
+    const int tile = blockIdx.z, a = blockIdx.y / TB, c = blockIdx.y % TB, which = blockIdx.x & 1;
+    const int I = tile_lo + tile, J = I + delta;
+    const int s = I * TB + 1 + a, t = J * TB + 1 + c;
+    if (s > n || t > n || s > t || (which == 1 && t == n)) return;
+    const double *row_src = which == 0 ? p.C + cell_index(n, s, t) * p.pitch : p.A + a_index(s, t) * p.pitch;
+    double *packed = buf + ((((int64_t)tile * 2 + which) * TB + a) * TB + c) * W;
+    double *row = const_cast<double *>(row_src);
+    for (int m = (blockIdx.x >> 1) * blockDim.x + threadIdx.x; m < W; m += (gridDim.x >> 1) * blockDim.x) {
+        if (unpack)
+            row[m] = packed[m];
+        else
+            packed[m] = row[m];
+    }
+}
+
+int tiled_pack(const Problem &p, int delta, int tile_lo, int tile_hi, double *buf, int unpack, cudaStream_t st) {
+    if (tile_hi <= tile_lo) return 0;
+    dim3 grid(2 * 4, tiled::TB * tiled::TB, tile_hi - tile_lo);
+    k_tile_pack<<<grid, 256, 0, st>>>(p, delta, tile_lo, buf, unpack);
+    return 1;
 }
 
 }  // namespace rotor

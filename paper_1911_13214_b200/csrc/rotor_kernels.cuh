@@ -29,8 +29,20 @@ struct BatchArgs {
 size_t batch_slot_bytes(int L_max, int S);
 void launch_batch(const BatchArgs &b, int n_slots, cudaStream_t st);
 
-// Tiled fill (rotor_tiled.cu). Returns the number of kernels launched.
+// Tiled fill (rotor_fill_tiled.cu). Returns the number of kernels launched (-1: setup error).
 int launch_fill_tiled(const Problem &p, cudaStream_t st);
 size_t tiled_extra_bytes(int L, int S);
+
+// Pieces of the tiled fill for a sharded (multi-rank) solve.
+struct TiledCtx {
+    alignas(64) unsigned char tmA[128];  // CUtensorMap of the A table
+    alignas(64) unsigned char tmC[128];  // CUtensorMap of the C table
+    int phase_id;                        // leaf launches so far (look-back flag epochs)
+};
+int tiled_nb(int n);  // number of TB-stage blocks
+int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st);
+int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int tile_hi, cudaStream_t st);
+size_t tiled_tile_bytes(int S);
+int tiled_pack(const Problem &p, int delta, int tile_lo, int tile_hi, double *buf, int unpack, cudaStream_t st);
 
 }  // namespace rotor

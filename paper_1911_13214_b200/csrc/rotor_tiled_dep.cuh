@@ -51,10 +51,9 @@ __device__ __forceinline__ double ld(const double *p, bool fresh) { return fresh
 // loads of split k+1 are issued before the arithmetic of split k.
 constexpr int PH = SB / 2;  // columns per lane
 
-__global__ void __launch_bounds__(DEP_THREADS, 3) k_sub_product(Problem p, int delta, int e) {
+__global__ void __launch_bounds__(DEP_THREADS, 3) k_sub_product(Problem p, int delta, int e, int tile_lo,
+                                                                int ntiles) {
     const int n = p.n, S = p.S;
-    const int nb = (n + TB - 1) / TB;
-    const int ntiles = nb - delta;
     const int cnt = sub_count(delta, e);
     const int n_mg = (S + 1 + 15) / 16;
     const int item = (blockIdx.x * DEP_THREADS + threadIdx.x) >> 5;
@@ -65,7 +64,7 @@ __global__ void __launch_bounds__(DEP_THREADS, 3) k_sub_product(Problem p, int d
     const int rest = item / n_mg;
     int alpha, gamma;
     sub_at(delta, e, rest % cnt, alpha, gamma);
-    const int I = rest / cnt, J = I + delta;
+    const int I = tile_lo + rest / cnt, J = I + delta;
     const int i0 = I * TB + 1, j0 = J * TB + 1;
     const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
     // split ranges and the freshness of their operands
@@ -265,7 +264,8 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
 constexpr int LEAF_M = 128;
 
 template <bool DIAG>
-__global__ void __launch_bounds__(LEAF_M, 4) k_sub_leaf(Problem p, int delta, int e, int *flags, int phase_id) {
+__global__ void __launch_bounds__(LEAF_M, 4) k_sub_leaf(Problem p, int delta, int e, int *flags, int phase_id,
+                                                        int tile_lo) {
     const int n = p.n;
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int cnt = sub_count(delta, e);
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(LEAF_M, 4) k_sub_leaf(Problem p, int delta, in
     const int sub = blockIdx.x / n_chunks;  // tile I * cnt + sub-tile index
     int alpha, gamma;
     sub_at(delta, e, sub % cnt, alpha, gamma);
-    const int I = sub / cnt;
+    const int I = tile_lo + sub / cnt;
     const int m = q * LEAF_M + threadIdx.x;
     int *my_flags = flags + (int64_t)sub * n_chunks;
     (void)n;
@@ -327,7 +327,8 @@ constexpr bool LEAF_USE_SMEM = false;
 constexpr int NPAIR = SB * (SB + 1) / 2;
 constexpr size_t LEAF_SMEM = (size_t)(NPAIR + SB * SB) * LEAF_M * 8;
 
-__global__ void __launch_bounds__(LEAF_M) k_sub_leaf_smem(Problem p, int delta, int e, int *flags, int phase_id) {
+__global__ void __launch_bounds__(LEAF_M) k_sub_leaf_smem(Problem p, int delta, int e, int *flags, int phase_id,
+                                                          int tile_lo) {
     extern __shared__ double lsm[];
     double *RS_ = lsm;                   // [NPAIR][LEAF_M]
     double *CS_ = lsm + NPAIR * LEAF_M;  // [SB][SB][LEAF_M]
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(LEAF_M) k_sub_leaf_smem(Problem p, int delta, 
     const int sub = blockIdx.x / n_chunks;
     int alpha, gamma;
     sub_at(delta, e, sub % cnt, alpha, gamma);
-    const int I = sub / cnt, J = I + delta;
+    const int I = tile_lo + sub / cnt, J = I + delta;
     const int i0 = I * TB + 1, j0 = J * TB + 1;
     const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
     const int ea = s0 + SB - 1;
@@ -425,10 +426,12 @@ inline size_t leaf_flag_bytes(int L, int S) {
 // Launch the dependent phase of tile diagonal delta; returns the launch count.
 // phase_id: running counter of leaf launches in this solve (flags zeroed at
 // the start of the fill, so phase ids >= 1 never match stale values).
-inline int launch_dependent(const Problem &p, int delta, cudaStream_t st, int *flags, int &phase_id) {
-    const int n = p.n;
-    const int nb = (n + TB - 1) / TB;
-    const int ntiles = nb - delta;
+// Tiles I in [tile_lo, tile_hi) of the diagonal (all of them in a single-GPU solve;
+// a rank's share in a sharded one).
+inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_hi, cudaStream_t st, int *flags,
+                            int &phase_id) {
+    const int ntiles = tile_hi - tile_lo;
+    if (ntiles <= 0) return 0;
     const int n_mg = (p.S + 1 + 15) / 16;  // product: a warp per (sub-tile, 16 m)
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int phases = delta == 0 ? NSB : 2 * NSB - 1;
@@ -446,15 +449,16 @@ inline int launch_dependent(const Problem &p, int delta, cudaStream_t st, int *f
             has_product = !(cnt == 1 && a == NSB - 1 && g == 0);
         }
         if (has_product) {
-            k_sub_product<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e);
+            k_sub_product<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
             launches++;
         }
+        const int lb = ntiles * cnt * n_chunks;
         if (delta == 0 && e == 0)
-            k_sub_leaf<true><<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
+            k_sub_leaf<true><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else if (LEAF_USE_SMEM)
-            k_sub_leaf_smem<<<ntiles * cnt * n_chunks, LEAF_M, LEAF_SMEM, st>>>(p, delta, e, flags, ++phase_id);
+            k_sub_leaf_smem<<<lb, LEAF_M, LEAF_SMEM, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else
-            k_sub_leaf<false><<<ntiles * cnt * n_chunks, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id);
+            k_sub_leaf<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         launches++;
     }
     return launches;

@@ -13,6 +13,133 @@ from __future__ import annotations
 import numpy as np
 
 
+def tile_ranges(n_tiles: int, world: int):
+    """Contiguous, balanced tile ranges [lo, hi) per rank (the first n % world ranks get one more)."""
+    base, extra = divmod(n_tiles, world)
+    out, lo = [], 0
+    for r in range(world):
+        hi = lo + base + (1 if r < extra else 0)
+        out.append((lo, hi))
+        lo = hi
+    return out
+
+
+class CudaShardEngine:
+    """This rank's share of a sharded single-table solve (rotor_sharded_* through the binding)."""
+
+    def __init__(self, chain, mem_limit: int, slots: int, device=None, stream=None, **opts):
+        import numpy as np
+        import torch
+
+        from . import Shard, max_ops, tile_blocks, tile_bytes, workspace_bytes
+
+        self.torch = torch
+        self.dev = torch.device("cuda") if device is None else torch.device(device)
+        self.stream = stream
+        self.L, self.S = int(chain.L), int(slots)
+        self.d_chain = {k: torch.from_numpy(np.asarray(getattr(chain, k)).astype(
+            np.float64 if k in ("uf", "ub") else np.int64)).to(self.dev) for k in ("uf", "ub", "wx", "wbx", "wy", "of", "ob")}
+        self.ws = torch.empty(workspace_bytes(self.L, self.S, kernel="tiled"), dtype=torch.uint8, device=self.dev)
+        self._args = (mem_limit, opts)
+        self.shard = Shard(self.d_chain, self.L, mem_limit, self.S, self.ws, stream=stream, **opts)
+        self.nb = tile_blocks(self.L)
+        self.tile_bytes = tile_bytes(self.S)
+        self.cap_ops = max_ops(self.L)
+        self._bufs = {}
+
+    def restart(self):
+        """A fresh solve in the same workspace (precompute, leaf, flags again)."""
+        from . import Shard
+
+        self.shard.close()
+        mem_limit, opts = self._args
+        self.shard = Shard(self.d_chain, self.L, mem_limit, self.S, self.ws, stream=self.stream, **opts)
+
+    def buffer(self, name: str, n_tiles: int):
+        need = max(1, n_tiles) * self.tile_bytes
+        b = self._bufs.get(name)
+        if b is None or b.numel() < need:
+            b = self.torch.empty(need, dtype=self.torch.uint8, device=self.dev)
+            self._bufs[name] = b
+        return b[:need]
+
+    def step(self, delta, lo, hi):
+        self.shard.step(delta, lo, hi, stream=self.stream)
+
+    def pack(self, delta, lo, hi, buf):
+        self.shard.pack(delta, lo, hi, buf, unpack=False, stream=self.stream)
+
+    def unpack(self, delta, lo, hi, buf):
+        self.shard.pack(delta, lo, hi, buf, unpack=True, stream=self.stream)
+
+    def finish(self):
+        t = self.torch
+        out = dict(cost=t.empty(1, dtype=t.float64, device=self.dev),
+                   ops=t.empty((self.cap_ops, 2), dtype=t.int32, device=self.dev),
+                   n_ops=t.empty(1, dtype=t.int64, device=self.dev), status=t.empty(1, dtype=t.int32, device=self.dev))
+        self.shard.finish(out, stream=self.stream)
+        t.cuda.synchronize(self.dev)
+        k = int(out["n_ops"].item())
+        return int(out["status"].item()), float(out["cost"].item()), out["ops"][: max(k, 0)].cpu().numpy()
+
+
+def solve_sharded(engine, group=None):
+    """one table sharded over the ranks of `group`.
+
+    Per tile diagonal delta (every tile of which depends only on smaller
+    diagonals): each rank computes a contiguous range of the tiles,
+    packs them, the ranks all-gather the packed tiles (NCCL over NVLink on
+    GPUs, gloo in the CPU tests), and every rank unpacks the others' tiles, so
+    each rank ends with the full table and runs Algorithm 2 itself.
+    `engine` provides nb, tile_bytes, step, pack, unpack, buffer, finish.
+    """
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    tb = engine.tile_bytes
+    for delta in range(engine.nb):
+        ranges = tile_ranges(engine.nb - delta, world)
+        lo, hi = ranges[rank]
+        engine.step(delta, lo, hi)
+        if world == 1:
+            continue
+        cap = max(h - l for l, h in ranges)
+        send = engine.buffer("send", cap)
+        engine.pack(delta, lo, hi, send)
+        recv = engine.buffer("recv", cap * world)
+        dist.all_gather_into_tensor(recv, send, group=group)
+        for r, (l, h) in enumerate(ranges):
+            if r != rank and h > l:
+                engine.unpack(delta, l, h, recv[r * cap * tb: (r * cap + (h - l)) * tb])
+    return engine.finish()
+
+
+def solve_sharded_virtual(engines):
+    """The same schedule with len(engines) ranks emulated in one process (the
+    all-gather becomes direct unpacks of the other engines' send buffers)."""
+    world = len(engines)
+    nb = engines[0].nb
+    tb = engines[0].tile_bytes
+    for delta in range(nb):
+        ranges = tile_ranges(nb - delta, world)
+        for r, e in enumerate(engines):
+            e.step(delta, *ranges[r])
+        if world == 1:
+            continue
+        cap = max(h - l for l, h in ranges)
+        sends = []
+        for r, e in enumerate(engines):
+            s = e.buffer("send", cap)
+            e.pack(delta, *ranges[r], s)
+            sends.append(s)
+        for r, e in enumerate(engines):
+            for q, (l, h) in enumerate(ranges):
+                if q != r and h > l:
+                    e.unpack(delta, l, h, sends[q][: (h - l) * tb])
+    return [e.finish() for e in engines]
+
+
 def problem_weights(chains, limits, slots: int):
     """Nominal transitions of every (chain, limit) problem, row-major by chain."""
     from . import transitions
