@@ -30,9 +30,9 @@ namespace rotor {
 namespace tiled {
 
 constexpr int TB = 32;      // tile edge in stages
-constexpr int KC = 8;       // splits per pipeline stage
+constexpr int KC = 4;       // splits per pipeline stage
 constexpr int TM = 16;      // m values per CTA (middle kernel)
-constexpr int STAGES = 3;   // TMA pipeline depth
+constexpr int STAGES = 6;   // TMA pipeline depth (5 stages in flight while one is consumed)
 constexpr int CONSUMERS = 256;
 constexpr int THREADS = CONSUMERS;
 constexpr int RS = 8, RT = 8;            // register tile (s x t) per consumer thread
@@ -98,13 +98,15 @@ constexpr int INT_MIN_COLS = 0;  // register-tile columns j >= RT - INT_MIN_COLS
 // ---------------------------------------------------------------------------
 // Middle phase of tile diagonal delta >= 2: partial(s,t,m) = min over s' in
 // blocks I+1..J-1 of A(s,s'-1,m) + C(s',t,m-wx[s'-1]); written into C.
-// grid = (ceil((S+1)/TM), tiles); 8 warps (thread = one m, an 8x8 (s,t)
-// register tile); thread 0 also issues the 16 TMA boxes of each stage
-// (full/empty mbarrier ring, no block-wide barrier in the main loop).
+// Persistent: one CTA per SM walks the work items (tile, 16-m chunk)
+// blockIdx.x, +gridDim.x, ...; the TMA ring runs across item boundaries, so
+// the loads of the next item overlap the epilogue of the current one.
+// 8 warps (thread = one m, an 8x8 (s,t) register tile); thread 0 also issues
+// the 2*KC TMA boxes of each stage (full/empty mbarrier ring).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC, Problem p,
-                  int delta, int tile_lo) {
+                  int delta, int tile_lo, int n_tiles) {
     extern __shared__ __align__(1024) double smem[];  // no static smem: the dynamic base is aligned
     double *As = smem;                     // [STAGES][KC][TB][TM]
     double *Bs = smem + STAGES * A_STAGE;  // [STAGES][KC][TB][TMB]
@@ -112,19 +114,25 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t *empty = full + STAGES;
     int *soff = reinterpret_cast<int *>(empty + STAGES);  // [STAGES][KC] column offset of each C box
 
-    const int I = tile_lo + blockIdx.y, J = I + delta;
-    const int i0 = I * TB + 1, j0 = J * TB + 1, i1 = i0 + TB;
-    const int m0 = blockIdx.x * TM;
     const int n = p.n;
+    const int n_mc = (p.S + 1 + TM - 1) / TM;
+    const int n_items = n_tiles * n_mc;
+    if ((int)blockIdx.x >= n_items) return;
+    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
     const int iters = (delta - 1) * TB / KC;
+    const int total = my_items * iters;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
 
     // TMA producer: lane 0 of warp 0 (no dedicated warp: the 8x8 register tile
     // needs ~240 registers, which leaves no room for a ninth warp)
-    auto issue = [&](int it) {
-        const int st = it % STAGES;
-        const int sp0 = i1 + it * KC;
+    auto issue = [&](int gi) {  // gi: position in this CTA's (item, k-step) sequence
+        const int st = gi % STAGES;
+        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        const int i0 = I * TB + 1, j0 = J * TB + 1;
+        const int m0 = (item % n_mc) * TM;
+        const int sp0 = i0 + TB + (gi % iters) * KC;
         // column offsets first: the expect_tx arrive (release) orders them
         // before the consumers' full-barrier wait (acquire)
         for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - p.wx[sp0 + k - 1], -kPad) + kPad) & 1;
@@ -150,11 +158,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     __syncthreads();
     if (tid == 0)
-        for (int it = 0; it < STAGES && it < iters; it++) issue(it);
+        for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);
 
     const int mi = tid & 15;
     const int g = tid >> 4;
     const int sg = g >> 2, tg = g & 3;
+    for (int kl = 0; kl < my_items; kl++) {
     double acc[RS][RT];
 #pragma unroll
     for (int i = 0; i < RS; i++)
@@ -162,8 +171,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 0; j < RT; j++) acc[i][j] = INFINITY;
 
     for (int it = 0; it < iters; it++) {
-        const int st = it % STAGES;
-        mbar_wait(&full[st], (uint32_t)((it / STAGES) & 1));
+        const int gi = kl * iters + it;
+        const int st = gi % STAGES;
+        mbar_wait(&full[st], (uint32_t)((gi / STAGES) & 1));
         const double *a_s = As + st * A_STAGE + (sg * RS) * TM + mi;
         const double *b_s = Bs + st * B_STAGE + (tg * RT) * TMB + mi;
 #pragma unroll
@@ -183,13 +193,16 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading stage st
-        if (tid == 0 && it + STAGES < iters) {   // refill st once all 8 warps released it
-            mbar_wait(&empty[st], (uint32_t)((it / STAGES) & 1));
-            issue(it + STAGES);
+        if (tid == 0 && gi + STAGES < total) {   // refill st once all 8 warps released it
+            mbar_wait(&empty[st], (uint32_t)((gi / STAGES) & 1));
+            issue(gi + STAGES);
         }
     }
 
-    const int m = m0 + mi;
+    const int item = (int)blockIdx.x + kl * (int)gridDim.x;
+    const int I = tile_lo + item / n_mc, J = I + delta;
+    const int i0 = I * TB + 1, j0 = J * TB + 1;
+    const int m = (item % n_mc) * TM + mi;
     if (m <= p.S) {
 #pragma unroll
         for (int i = 0; i < RS; i++) {
@@ -201,6 +214,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
     }
+    }  // items
 }
 
 #include "rotor_tiled_dep.cuh"
@@ -271,10 +285,17 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
     if (tile_hi <= tile_lo) return 0;
     int launches = 0;
     if (delta >= 2) {
-        dim3 grid((p.S + 1 + TM - 1) / TM, tile_hi - tile_lo);
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        }
+        const int n_items = (tile_hi - tile_lo) * ((p.S + 1 + TM - 1) / TM);
+        const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
         k_tile_middle<<<grid, THREADS, SMEM_BYTES, st>>>(*reinterpret_cast<const CUtensorMap *>(ctx->tmA),
                                                          *reinterpret_cast<const CUtensorMap *>(ctx->tmC), p,
-                                                         delta, tile_lo);
+                                                         delta, tile_lo, tile_hi - tile_lo);
         launches++;
     }
     return launches + launch_dependent(p, delta, tile_lo, tile_hi, st, p.flags, ctx->phase_id);
