@@ -33,9 +33,10 @@ constexpr int TB = 32;      // tile edge in stages
 constexpr int KC = 4;       // splits per pipeline stage
 constexpr int TM = 16;      // m values per CTA (middle kernel)
 constexpr int STAGES = 6;   // TMA pipeline depth (5 stages in flight while one is consumed)
-constexpr int CONSUMERS = 256;
+constexpr int CONSUMERS = 512;  // 16 warps: two per scheduler slot more than 8 hide the DADD->DSETP->FSEL chain
 constexpr int THREADS = CONSUMERS;
-constexpr int RS = 8, RT = 8;            // register tile (s x t) per consumer thread
+constexpr int RS = 4, RT = 8;            // register tile (s x t) per consumer thread (<= 128 registers)
+static_assert((TB / RS) * (TB / RT) * TM == CONSUMERS, "one thread per (m, register tile)");
 // A TMA box must start on a 16-byte boundary of the row (an odd fp64 start
 // column faults with "illegal instruction", scripts/tma_probe.cu): the shifted
 // C boxes start at the even column below the wanted one and are TMB = TM + 2
@@ -101,7 +102,7 @@ constexpr int INT_MIN_COLS = 0;  // register-tile columns j >= RT - INT_MIN_COLS
 // Persistent: one CTA per SM walks the work items (tile, 16-m chunk)
 // blockIdx.x, +gridDim.x, ...; the TMA ring runs across item boundaries, so
 // the loads of the next item overlap the epilogue of the current one.
-// 8 warps (thread = one m, an 8x8 (s,t) register tile); thread 0 also issues
+// 16 warps (thread = one m, a 4x8 (s,t) register tile); thread 0 also issues
 // the 2*KC TMA boxes of each stage (full/empty mbarrier ring).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(THREADS, 1)
