@@ -125,8 +125,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tid = threadIdx.x;
     const int lane = tid & 31;
 
-    // TMA producer: lane 0 of warp 0 (no dedicated warp: the 8x8 register tile
-    // needs ~240 registers, which leaves no room for a ninth warp)
+    // TMA producer: lane 0 of warp 0 (no dedicated warp: 16 warps x 128
+    // registers already fill the register file)
     auto issue = [&](int gi) {  // gi: position in this CTA's (item, k-step) sequence
         const int st = gi % STAGES;
         const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
@@ -158,7 +158,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    if (tid == 0)
+    // The producer is lane 0 of the LAST warp: the warp scheduler favours the
+    // highest warp id, so the refills are not delayed behind the consumers
+    // (with warp 0 as producer ~19% of the warp time was spent waiting for
+    // TMA data, profiles/r01_tiled_v4.md).
+    constexpr int PRODUCER = CONSUMERS - 32;
+    if (tid == PRODUCER)
         for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);
 
     const int mi = tid & 15;
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done reading stage st
-        if (tid == 0 && gi + STAGES < total) {   // refill st once all 8 warps released it
+        if (tid == PRODUCER && gi + STAGES < total) {  // refill st once every warp released it
             mbar_wait(&empty[st], (uint32_t)((gi / STAGES) & 1));
             issue(gi + STAGES);
         }

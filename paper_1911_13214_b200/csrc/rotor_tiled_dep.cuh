@@ -262,9 +262,10 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
 // has done the rows below.  CTAs of lower chunks have lower blockIdx and never
 // wait on higher ones, so the chain always progresses (decoupled look-back).
 constexpr int LEAF_M = 128;
+constexpr int LEAF_MIN_BLOCKS = 8;  // 32 warps/SM for the latency-bound leaf (<= 64 registers)
 
 template <bool DIAG>
-__global__ void __launch_bounds__(LEAF_M, 4) k_sub_leaf(Problem p, int delta, int e, int *flags, int phase_id,
+__global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf(Problem p, int delta, int e, int *flags, int phase_id,
                                                         int tile_lo) {
     const int n = p.n;
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
