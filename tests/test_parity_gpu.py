@@ -139,6 +139,23 @@ def test_edge_cases(R, oracle_mod, kernel):
     assert tr.status == R.ETRUNC and tr.n_ops == full.n_ops and tr.op_list() == full.op_list()[:5]
 
 
+@pytest.mark.parametrize("L", [30, 31, 32, 33, 63, 64, 71, 95, 96, 127, 160])
+def test_tiled_block_boundaries(R, oracle_mod, L):
+    """Chains whose length straddles the 32-stage tiles / 8-stage sub-tiles of the tiled
+    fill (partial last block, exact multiples, one stage over), with wide shifts (large
+    abar/a relative to the slot size) and a ragged S: full tables bit-exact, both modes."""
+    O = oracle_mod
+    rng = G.SplitMix64(1000 + L)
+    ch = G.random_chain(rng, L, real_times=True, big=True)
+    S = 37 + (L % 23)
+    M = max(1, int(sum(int(x) for x in ch.wbx) * 0.22))
+    check_against_oracle(R, O, ch, M, S, kernel="tiled")
+    check_against_oracle(R, O, ch, M, S, kernel="tiled", restricted=True)
+    # integer times: ties everywhere (the fill keeps no argmin; Algorithm 2 re-derives it)
+    ch2 = G.tiny_chain(rng, L, size_max=3, time_max=2, allow_zero_time=True)
+    check_against_oracle(R, O, ch2, 24, 24, kernel="tiled")
+
+
 def test_device_resident_path(R, oracle_mod):
     import torch
 
