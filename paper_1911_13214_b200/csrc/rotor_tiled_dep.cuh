@@ -170,6 +170,7 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
     double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
 
     if (DIAG) {  // diagonal sub-tile (delta = 0, e = 0): cells (s, s+1..ea), splits s' in (s, t]
+        if (s == n) return;  // the last stage's row has no cell right of its leaf
         const double leaf = p.A[a_index(s, s) * pitch + m];  // the leaf (k_leaf, an earlier launch)
 #pragma unroll
         for (int c = 0; c < SB; c++)  // AR[r + 1] = leaf, with compile-time register indices

@@ -23,7 +23,7 @@ chains, limits, S = G.config5(n_limits=3)
 costs, status, n_ops, ops = R.solve_batch(chains[:3], [l[:3] for l in limits[:3]], 60, with_ops=True)
 print("batch", costs.shape, status.tolist())
 EOF
-for tool in memcheck racecheck synccheck initcheck; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 20 python /tmp/san_run.py > "$OUT/$tool.log" 2>&1
+for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
+  timeout 900 compute-sanitizer --tool $tool --print-limit 200 python /tmp/san_run.py > "$OUT/$tool.log" 2>&1
   echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' "$OUT/$tool.log" | tail -1)"
 done
