@@ -288,6 +288,8 @@ def run_sharded(args):
 
     import chaingen as G
 
+    for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+        os.environ.setdefault(k, v)  # single-rank use without torchrun
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -364,8 +366,9 @@ def run_ours(args):
 
     if args.config == 5:
         return run_batched(args)
-    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.mode == "sharded":
-        return run_sharded(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.mode == "sharded" and (world > 1 or os.environ.get("ROTOR_FORCE_SHARDED") == "1"):
+        return run_sharded(args)  # ROTOR_FORCE_SHARDED=1: the sharded path on a single rank (a test hook)
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)

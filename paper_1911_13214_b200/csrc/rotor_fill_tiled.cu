@@ -83,6 +83,13 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, i
         : "memory");
 }
 
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap *map, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
+
 __device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
 
 // The same exact min on the integer pipe: non-negative doubles (every
@@ -125,28 +132,43 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tid = threadIdx.x;
     const int lane = tid & 31;
 
-    // TMA producer: lane 0 of warp 0 (no dedicated warp: 16 warps x 128
-    // registers already fill the register file)
-    auto issue = [&](int gi) {  // gi: position in this CTA's (item, k-step) sequence
-        const int st = gi % STAGES;
+    // TMA producer (no dedicated warp: 16 warps x 128 registers already fill
+    // the register file).  Step gi of this CTA's (item, k-step) sequence loads,
+    // for k < KC: A cells (i0..i0+TB-1, c = sp0+k-1) and C cells
+    // (sp = sp0+k, j0..j0+TB-1) at m - wx[sp-1].  A C window starting below
+    // -kPad lies wholly under m = wx[sp-1] <= m_null(s,t): every cell it feeds
+    // is gated and the clamped values are never used (DESIGN Q6).
+    auto step_coords = [&](int gi, int &m0, int &i0, int &j0, int &sp0) {
         const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
         const int I = tile_lo + item / n_mc, J = I + delta;
-        const int i0 = I * TB + 1, j0 = J * TB + 1;
-        const int m0 = (item % n_mc) * TM;
-        const int sp0 = i0 + TB + (gi % iters) * KC;
+        i0 = I * TB + 1;
+        j0 = J * TB + 1;
+        m0 = (item % n_mc) * TM;
+        sp0 = i0 + TB + (gi % iters) * KC;
+    };
+    auto issue = [&](int gi) {
+        const int st = gi % STAGES;
+        int m0, i0, j0, sp0;
+        step_coords(gi, m0, i0, j0, sp0);
         // column offsets first: the expect_tx arrive (release) orders them
         // before the consumers' full-barrier wait (acquire)
         for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - p.wx[sp0 + k - 1], -kPad) + kPad) & 1;
         mbar_expect_tx(&full[st], (uint32_t)((A_STAGE + B_STAGE) * 8));
-        for (int k = 0; k < KC; k++) {  // A cells (i0..i0+TB-1, c), c = sp0+k-1
+        for (int k = 0; k < KC; k++)
             tma_load_2d(As + st * A_STAGE + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
-        }
-        for (int k = 0; k < KC; k++) {  // C cells (sp, j0..j0+TB-1) at m - wx[sp-1]
+        for (int k = 0; k < KC; k++) {
             const int sp = sp0 + k;
-            // a window starting below -kPad lies wholly under m = wx[sp-1] <= m_null(s,t):
-            // every cell it feeds is gated, the clamped values are never used (DESIGN Q6)
             const int c0 = max(m0 - p.wx[sp - 1], -kPad) + kPad;
             tma_load_2d(Bs + st * B_STAGE + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp, j0), &full[st]);
+        }
+        // warm L2 for the step that will refill this slot next time around
+        if (gi + STAGES < total) {
+            step_coords(gi + STAGES, m0, i0, j0, sp0);
+            for (int k = 0; k < KC; k++) {
+                tma_prefetch_2d(&tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1));
+                const int sp = sp0 + k;
+                tma_prefetch_2d(&tmC, (max(m0 - p.wx[sp - 1], -kPad) + kPad) & ~1, (int)cell_index(n, sp, j0));
+            }
         }
     };
 
