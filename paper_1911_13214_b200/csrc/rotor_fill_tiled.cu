@@ -161,15 +161,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int c0 = max(m0 - p.wx[sp - 1], -kPad) + kPad;
             tma_load_2d(Bs + st * B_STAGE + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp, j0), &full[st]);
         }
-        // warm L2 for the step that will refill this slot next time around
-        if (gi + STAGES < total) {
-            step_coords(gi + STAGES, m0, i0, j0, sp0);
-            for (int k = 0; k < KC; k++) {
-                tma_prefetch_2d(&tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1));
-                const int sp = sp0 + k;
-                tma_prefetch_2d(&tmC, (max(m0 - p.wx[sp - 1], -kPad) + kPad) & ~1, (int)cell_index(n, sp, j0));
-            }
-        }
+        // (an L2 prefetch of the next ring's boxes, cp.async.bulk.prefetch.tensor,
+        // measured slower: 204 vs 164 ms of middle time at config 4 — not used)
     };
 
     if (tid == 0) {
