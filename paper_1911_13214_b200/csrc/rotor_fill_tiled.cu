@@ -22,6 +22,9 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
+#include <limits.h>
 
 #include "rotor_common.cuh"
 #include "rotor_kernels.cuh"

@@ -292,11 +292,152 @@ __global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf(Problem p,
         }
         leaf_row<DIAG>(p, delta, e, alpha, gamma, I, r, m);
         __syncthreads();  // every thread of this chunk finished row r
-        if (threadIdx.x == 0) {
-            __threadfence();
+        if (threadIdx.x == 0) {  // release (cumulative over the barrier): the chunk's row r is visible
             const int done = (phase_id << 4) | (SB - r);
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(my_flags + q), "r"(done) : "memory");
         }
+    }
+}
+
+// Per-sub-tile scalars of an off-diagonal leaf, staged once in shared memory
+// so the row path has no dependent global round trip.
+struct LeafTab {
+    int mnull[SB][SB], mall[SB][SB];  // m_null / m_all of cell (s0+r, t0+c); INT_MAX: no cell / gate shut
+    int wxl[SB];                      // wxl[j] = wx[s0+j-1]: shift of the left split s' = s0+j
+    int wxr[SB];                      // wxr[c] = wx[t0+c-1]: shift of the right split s' = t0+c
+    int wbx[SB];                      // wbx[s0+r]: F_all shift of row r
+    double w[SB], Ps[SB], Pt[SB];     // w[s0+r], P[s0+r-1], P[t0+c]
+    int q_lo;                         // lowest m-chunk a shifted read of a row below can reach
+};
+
+__device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, int m0, int chunk_m, LeafTab &T) {
+    const int n = p.n;
+    if (threadIdx.x < SB * SB) {
+        const int rr = threadIdx.x / SB, cc = threadIdx.x % SB, ss = s0 + rr, tt = t0 + cc;
+        const bool ok = ss <= n && tt <= n;  // ss < tt in an off-diagonal sub-tile
+        T.mnull[rr][cc] = ok ? m_null(p, ss, tt) : INT_MAX;
+        T.mall[rr][cc] = ok && !p.restricted ? m_all(p, ss, tt) : INT_MAX;
+        if (cc == 0) {
+            const bool row = ss < n;  // rows s < t <= n
+            T.wxl[rr] = rr > 0 && ss <= n ? p.wx[ss - 1] : 0;
+            T.wxr[rr] = t0 + rr <= n ? p.wx[t0 + rr - 1] : 0;
+            T.wbx[rr] = row ? p.wbx[ss] : 0;
+            T.w[rr] = row ? p.w[ss] : 0.0;
+            T.Ps[rr] = ss <= n ? p.P[ss - 1] : 0.0;
+            T.Pt[rr] = p.P[min(t0 + rr, n)];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int wmax = 0;
+        for (int k = 0; k < SB; k++) wmax = max(wmax, max(T.wxl[k], T.wbx[k]));
+        T.q_lo = m0 - wmax <= 0 ? 0 : (m0 - wmax) / chunk_m;
+    }
+    __syncthreads();
+}
+
+// Off-diagonal leaf row r at one m (thread = m), scalars from the table; the
+// same arithmetic as leaf_row<false>.
+template <int r>
+__device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T, bool fresh, bool partial, int s0,
+                                             int t0, int m) {
+    const int n = p.n;
+    const int64_t pitch = p.pitch;
+    const int s = s0 + r;
+    double AL[SB - 1];  // AL[k] = A(s, s + k): left split s' = s + k + 1 <= ea
+#pragma unroll
+    for (int k = 0; k < SB - 1; k++) AL[k] = (k < SB - 1 - r) ? ld(&p.A[a_index(s, s + k) * pitch + m], fresh) : INFINITY;
+    double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
+    AR[0] = __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]);
+    double B[SB], F[SB];
+    bool gate[SB];
+#pragma unroll
+    for (int c = 0; c < SB; c++) {
+        const int t = t0 + c;
+        gate[c] = m >= T.mnull[r][c];  // INT_MAX past the last stage
+        double best = INFINITY;
+        if (gate[c]) {
+            best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
+#pragma unroll
+            for (int k = 0; k < SB - 1; k++) {  // left: C of the rows below in this sub-tile
+                if (k >= SB - 1 - r) break;
+                const int j = r + k + 1;  // s' = s0 + j
+                const double cv = __ldcg(&p.C[cell_index(n, s0 + j, t) * pitch + (m - T.wxl[j])]);
+                best = dmin(best, __dadd_rn(AL[k], cv));
+            }
+        }
+        B[c] = best;
+        F[c] = m >= T.mall[r][c]
+                   ? __dadd_rn(T.w[r], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - T.wbx[r])]))
+                   : INFINITY;
+    }
+#pragma unroll
+    for (int c = 0; c < SB; c++) {
+        const int t = t0 + c;
+        if (t > n) break;
+        double c1 = INFINITY;
+        if (gate[c]) {
+            double best = B[c];
+#pragma unroll
+            for (int cq = 0; cq < SB; cq++) {  // right: s' = t0 + cq <= t
+                if (cq > c) break;
+                const double cv = ld(&p.C[cell_index(n, t0 + cq, t) * pitch + (m - T.wxr[cq])], fresh);
+                best = dmin(best, __dadd_rn(AR[cq], cv));
+            }
+            c1 = best;
+        }
+        const double cc = dmin(c1, F[c]);
+        p.C[cell_index(n, s, t) * pitch + m] = cc;
+        const double a = __dadd_rn(__dadd_rn(T.Pt[c], -T.Ps[r]), cc);
+        if (t < n) p.A[a_index(s, t) * pitch + m] = a;
+        AR[c + 1] = a;
+    }
+}
+
+__global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf_row(Problem p, int delta, int e, int *flags,
+                                                                        int phase_id, int tile_lo) {
+    __shared__ LeafTab T;
+    const int n = p.n;
+    const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
+    const int cnt = sub_count(delta, e);
+    const int q = blockIdx.x % n_chunks;
+    const int sub = blockIdx.x / n_chunks;
+    int alpha, gamma;
+    sub_at(delta, e, sub % cnt, alpha, gamma);
+    const int I = tile_lo + sub / cnt, J = I + delta;
+    const int s0 = I * TB + 1 + SB * alpha, t0 = J * TB + 1 + SB * gamma;
+    if (s0 > n || t0 > n) return;  // no cells (uniform over the sub-tile)
+    const int m = q * LEAF_M + threadIdx.x;
+    const bool fresh = (delta == 0);
+    const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
+    int *my_flags = flags + (int64_t)sub * n_chunks;
+    leaf_tab_fill(p, s0, t0, q * LEAF_M, LEAF_M, T);
+    const int q_lo = T.q_lo;
+    for (int r = SB - 1; r >= 0; r--) {
+        if (r < SB - 1) {
+            const int need = (phase_id << 4) | (SB - 1 - r);  // rows SB-1 .. r+1 done
+            for (int qq = q_lo + (int)threadIdx.x; qq < q; qq += LEAF_M) {
+                int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(my_flags + qq) : "memory");
+                } while (v < need);
+            }
+            __syncthreads();
+        }
+        if (s0 + r <= n && m <= p.S) switch (r) {  // compile-time row index: the row's loops fully unrolled
+                case 0: leaf_row_tab<0>(p, T, fresh, partial, s0, t0, m); break;
+                case 1: leaf_row_tab<1>(p, T, fresh, partial, s0, t0, m); break;
+                case 2: leaf_row_tab<2>(p, T, fresh, partial, s0, t0, m); break;
+                case 3: leaf_row_tab<3>(p, T, fresh, partial, s0, t0, m); break;
+                case 4: leaf_row_tab<4>(p, T, fresh, partial, s0, t0, m); break;
+                case 5: leaf_row_tab<5>(p, T, fresh, partial, s0, t0, m); break;
+                case 6: leaf_row_tab<6>(p, T, fresh, partial, s0, t0, m); break;
+                default: leaf_row_tab<7>(p, T, fresh, partial, s0, t0, m); break;
+            }
+        __syncthreads();
+        if (threadIdx.x == 0)
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(my_flags + q), "r"((phase_id << 4) | (SB - r))
+                         : "memory");
     }
 }
 
@@ -310,10 +451,7 @@ __device__ __forceinline__ void leaf_wait(const int *my_flags, int q, int need) 
 }
 
 __device__ __forceinline__ void leaf_publish(int *flag, int value) {
-    if (threadIdx.x == 0) {
-        __threadfence();
-        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
-    }
+    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
 }
 
 // Off-diagonal leaf with its operands in shared memory:
@@ -419,10 +557,161 @@ __global__ void __launch_bounds__(LEAF_M) k_sub_leaf_smem(Problem p, int delta, 
     }
 }
 
+// Off-diagonal leaf, column-parallel: CTA = LEAF_CM consecutive m x the SB
+// columns of one sub-tile, lane = (m, column c), c = lane % SB; the rows go
+// bottom-up as in k_sub_leaf (same look-back flags, chunks of LEAF_CM m).
+// What a lane keeps in registers for the whole sub-tile:
+//   Cr[cq] = C(t0+cq, t, m - wx[t0+cq-1])  right operand of split s' = t0+cq <= t
+//            (final before this launch: column sub-block gamma of (J,J));
+//   Lc[k]  = C(s0+k+1, t, m - wx[s0+k])    left operand of split s' = s0+k+1,
+//            the same for every row above s', loaded once right after row s'
+//            is done (this launch: behind the row barrier / look-back flags).
+// The row's own A operands A(s, t0+cq-1) travel along the row with a shuffle
+// inside the SB-lane group: lane cq-1 finishes its cell, then every lane
+// c >= cq takes the split s' = t0+cq.  Per row a lane loads only the
+// partial, the F_all operand, the new left operand and A(s, ·) (shared by
+// the group), instead of every split's C operand.
+constexpr int LEAF_CM = 32;             // m per CTA
+constexpr int LEAF_CT = LEAF_CM * SB;   // 256 threads
+
+__global__ void __launch_bounds__(LEAF_CT, 3) k_sub_leaf_col(Problem p, int delta, int e, int *flags, int phase_id,
+                                                              int tile_lo) {
+    const int n = p.n, S = p.S;
+    const int64_t pitch = p.pitch;
+    const int n_chunks = (S + 1 + LEAF_CM - 1) / LEAF_CM;
+    const int cnt = sub_count(delta, e);
+    const int q = blockIdx.x % n_chunks;
+    const int sub = blockIdx.x / n_chunks;
+    int alpha, gamma;
+    sub_at(delta, e, sub % cnt, alpha, gamma);
+    const int I = tile_lo + sub / cnt, J = I + delta;
+    const int i0 = I * TB + 1, j0 = J * TB + 1;
+    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
+    if (s0 > n || t0 > n) return;  // sub-tiles past the last stage: no cells (uniform for the whole sub-tile)
+    const int c = threadIdx.x % SB;
+    const int m0 = q * LEAF_CM;
+    const int m = m0 + threadIdx.x / SB;
+    const int t = t0 + c;
+    const bool live = m <= S && t <= n;  // this lane owns column t at m
+    const bool fresh = (delta == 0);     // right C and left A of this tile diagonal (see k_sub_leaf)
+    const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
+    int *my_flags = flags + (int64_t)sub * n_chunks;
+    // per-sub-tile tables in shared memory (no global round trip on the row path)
+    __shared__ int s_mnull[SB][SB], s_mall[SB][SB], s_wx[SB], s_wbx[SB];
+    __shared__ double s_w[SB], s_Ps[SB], s_Pt[SB];
+    __shared__ int s_qlo;
+    if (threadIdx.x < SB * SB) {
+        const int rr = threadIdx.x / SB, cc = threadIdx.x % SB, ss = s0 + rr, tt = t0 + cc;
+        const bool ok = ss <= n && tt <= n;  // ss < tt for off-diagonal sub-tiles
+        s_mnull[rr][cc] = ok ? m_null(p, ss, tt) : INT_MAX;
+        s_mall[rr][cc] = ok && !p.restricted ? m_all(p, ss, tt) : INT_MAX;
+        if (cc == 0) {
+            const bool row = ss < n;  // rows s < t <= n
+            s_wx[rr] = row ? p.wx[ss] : 0;    // shift of split s' = ss + 1
+            s_wbx[rr] = row ? p.wbx[ss] : 0;  // F_all shift of row ss
+            s_w[rr] = row ? p.w[ss] : 0.0;
+            s_Ps[rr] = ss <= n ? p.P[ss - 1] : 0.0;
+            s_Pt[rr] = p.P[min(t0 + rr, n)];
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {  // lowest chunk any shifted read of this sub-tile can reach
+        int wmax = 0;
+        for (int k = 0; k < SB; k++) wmax = max(wmax, max(s_wx[k], s_wbx[k]));
+        s_qlo = m0 - wmax <= 0 ? 0 : (m0 - wmax) / LEAF_CM;
+    }
+
+    double Cr[SB];
+#pragma unroll
+    for (int cq = 0; cq < SB; cq++) {
+        const int sp = t0 + cq;
+        const int w = cq <= c && live ? p.wx[sp - 1] : 0;
+        Cr[cq] = (live && cq <= c && m >= w) ? ld(&p.C[cell_index(n, sp, t) * pitch + (m - w)], fresh) : INFINITY;
+    }
+    double Lc[SB - 1];
+#pragma unroll
+    for (int k = 0; k < SB - 1; k++) Lc[k] = INFINITY;
+    __syncthreads();
+    const int q_lo = s_qlo;
+
+#pragma unroll
+    for (int r = SB - 1; r >= 0; r--) {
+        const int s = s0 + r;
+        if (r < SB - 1) {
+            const int need = (phase_id << 4) | (SB - 1 - r);  // rows SB-1 .. r+1 done
+            for (int qq = q_lo + (int)threadIdx.x; qq < q; qq += LEAF_CT) {
+                int v;
+                do {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(my_flags + qq) : "memory");
+                } while (v < need);
+            }
+            __syncthreads();
+        }
+        if (s <= n) {  // uniform over the CTA
+            // every load of the row in one round trip
+            const bool gate = live && m >= s_mnull[r][c];  // every shifted index >= 0 under it (DESIGN Q6)
+            const bool gall = live && m >= s_mall[r][c];   // F_all: row s+1 at m - wbx[s] >= 0
+            if (r < SB - 1) {  // row s+1 = s0+r+1 is complete at every m: its left operand for the rows above
+                const int w = s_wx[r];
+                Lc[r] = (live && m >= w) ? __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - w)]) : INFINITY;
+            }
+            const double fv = gall ? __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - s_wbx[r])]) : INFINITY;
+            double best = (gate && partial) ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
+            double al[SB - 1];
+#pragma unroll
+            for (int k = r; k < SB - 1; k++)  // left: s' = s0+k+1 in (s, ea], A(s, s'-1)
+                al[k] = gate ? ld(&p.A[a_index(s, s0 + k) * pitch + m], fresh) : INFINITY;
+            const double ar0 = live ? __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]) : INFINITY;  // A(s, t0-1)
+            if (gate) {
+#pragma unroll
+                for (int k = r; k < SB - 1; k++) best = dmin(best, __dadd_rn(al[k], Lc[k]));
+            }
+            const double F = gall ? __dadd_rn(s_w[r], fv) : INFINITY;
+            const double u = __dadd_rn(s_Pt[c], -s_Ps[r]);
+            double myA = INFINITY, cc = INFINITY;
+#pragma unroll
+            for (int cq = 0; cq < SB; cq++) {  // right: s' = t0+cq, operand A(s, t0+cq-1) from lane cq-1
+                const double a = cq == 0 ? ar0 : __shfl_sync(0xffffffffu, myA, cq - 1, SB);
+                if (gate && c >= cq) best = dmin(best, __dadd_rn(a, Cr[cq]));
+                if (c == cq) {
+                    cc = dmin(best, F);  // best = +inf when the m_null gate is closed
+                    myA = __dadd_rn(u, cc);
+                }
+            }
+            if (live) {
+                p.C[cell_index(n, s, t) * pitch + m] = cc;
+                if (t < n) p.A[a_index(s, t) * pitch + m] = myA;
+            }
+        }
+        __syncthreads();  // every lane of this chunk finished row r
+        if (threadIdx.x == 0)  // release (cumulative over the barrier): the chunk's row r is visible
+            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(my_flags + q), "r"((phase_id << 4) | (SB - r))
+                         : "memory");
+    }
+}
+
 // Flags of the leaf look-back: one int per (sub-tile of a phase, m-chunk).
 inline size_t leaf_flag_bytes(int L, int S) {
     const int nb = (L + 1 + TB - 1) / TB;
-    return (size_t)nb * NSB * ((S + 1 + LEAF_M - 1) / LEAF_M) * sizeof(int);
+    const int chunks = max((S + 1 + LEAF_M - 1) / LEAF_M, (S + 1 + LEAF_CM - 1) / LEAF_CM);
+    return (size_t)nb * NSB * chunks * sizeof(int);
+}
+
+// Off-diagonal leaf kernel: k_sub_leaf<false> (row: thread = m), k_sub_leaf_col
+// (thread = (m, column)) or k_sub_leaf_smem; ROTOR_LEAF=row|col|smem selects
+// one for measurements (default: the fastest measured, LEAF_VARIANT_DEFAULT).
+enum { LEAF_VARIANT_ROW = 0, LEAF_VARIANT_COL = 1, LEAF_VARIANT_SMEM = 2, LEAF_VARIANT_TAB = 3 };
+constexpr int LEAF_VARIANT_DEFAULT = LEAF_VARIANT_TAB;
+inline int leaf_variant() {
+    static const int v = [] {
+        const char *e = getenv("ROTOR_LEAF");
+        if (!e) return (int)LEAF_VARIANT_DEFAULT;
+        if (!strcmp(e, "col")) return (int)LEAF_VARIANT_COL;
+        if (!strcmp(e, "smem")) return (int)LEAF_VARIANT_SMEM;
+        if (!strcmp(e, "tab")) return (int)LEAF_VARIANT_TAB;
+        return (int)LEAF_VARIANT_ROW;
+    }();
+    return v;
 }
 
 // Launch the dependent phase of tile diagonal delta; returns the launch count.
@@ -436,6 +725,7 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
     if (ntiles <= 0) return 0;
     const int n_mg = (p.S + 1 + 15) / 16;  // product: a warp per (sub-tile, 16 m)
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
+    const int n_chunks_col = (p.S + 1 + LEAF_CM - 1) / LEAF_CM;
     const int phases = delta == 0 ? NSB : 2 * NSB - 1;
     int launches = 0;
     for (int e = 0; e < phases; e++) {
@@ -457,7 +747,11 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
         const int lb = ntiles * cnt * n_chunks;
         if (delta == 0 && e == 0)
             k_sub_leaf<true><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
-        else if (LEAF_USE_SMEM)
+        else if (leaf_variant() == LEAF_VARIANT_COL)
+            k_sub_leaf_col<<<ntiles * cnt * n_chunks_col, LEAF_CT, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
+        else if (leaf_variant() == LEAF_VARIANT_TAB)
+            k_sub_leaf_row<<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
+        else if (leaf_variant() == LEAF_VARIANT_SMEM)
             k_sub_leaf_smem<<<lb, LEAF_M, LEAF_SMEM, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else
             k_sub_leaf<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
