@@ -48,6 +48,9 @@ constexpr int TMB = TM + 2;
 constexpr int A_STAGE = KC * TB * TM;   // doubles [KC][TB s][TM]
 constexpr int B_STAGE = KC * TB * TMB;  // doubles [KC][TB t][TMB]
 constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * 8 + 2 * STAGES * 8 + STAGES * KC * 4 + 64;
+// The rest of the 227 KB holds a copy of wx (the producer's shift lookups stay
+// on chip: a global load there delays every refill by a memory round trip).
+constexpr int WX_SMEM_MAX = (int)((226 * 1024 - SMEM_BYTES) / 4);  // 1 KB kept for the static/system share
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -124,6 +127,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t *full = reinterpret_cast<uint64_t *>(Bs + STAGES * B_STAGE);
     uint64_t *empty = full + STAGES;
     int *soff = reinterpret_cast<int *>(empty + STAGES);  // [STAGES][KC] column offset of each C box
+    int *wx_s = soff + STAGES * KC;                       // wx[0..n) when n <= WX_SMEM_MAX
 
     const int n = p.n;
     const int n_mc = (p.S + 1 + TM - 1) / TM;
@@ -134,6 +138,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int total = my_items * iters;
     const int tid = threadIdx.x;
     const int lane = tid & 31;
+    const int *wxp = p.wx;
+    if (n <= WX_SMEM_MAX) {  // ordered before the producer's first use by the __syncthreads below
+        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
+        wxp = wx_s;
+    }
 
     // TMA producer (no dedicated warp: 16 warps x 128 registers already fill
     // the register file).  Step gi of this CTA's (item, k-step) sequence loads,
@@ -155,13 +164,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         step_coords(gi, m0, i0, j0, sp0);
         // column offsets first: the expect_tx arrive (release) orders them
         // before the consumers' full-barrier wait (acquire)
-        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - p.wx[sp0 + k - 1], -kPad) + kPad) & 1;
+        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 1;
         mbar_expect_tx(&full[st], (uint32_t)((A_STAGE + B_STAGE) * 8));
         for (int k = 0; k < KC; k++)
             tma_load_2d(As + st * A_STAGE + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
         for (int k = 0; k < KC; k++) {
             const int sp = sp0 + k;
-            const int c0 = max(m0 - p.wx[sp - 1], -kPad) + kPad;
+            const int c0 = max(m0 - wxp[sp - 1], -kPad) + kPad;
             tma_load_2d(Bs + st * B_STAGE + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp, j0), &full[st]);
         }
         // (an L2 prefetch of the next ring's boxes, cp.async.bulk.prefetch.tensor,
@@ -285,7 +294,8 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     static_assert(sizeof(CUtensorMap) <= sizeof(ctx->tmA), "tensor map storage");
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(k_tile_middle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES) !=
+        if (cudaFuncSetAttribute(k_tile_middle, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) !=
                 cudaSuccess ||
             cudaFuncSetAttribute(k_sub_leaf_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LEAF_SMEM) !=
                 cudaSuccess)
@@ -317,7 +327,8 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
         }
         const int n_items = (tile_hi - tile_lo) * ((p.S + 1 + TM - 1) / TM);
         const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
-        k_tile_middle<<<grid, THREADS, SMEM_BYTES, st>>>(*reinterpret_cast<const CUtensorMap *>(ctx->tmA),
+        const size_t smem = SMEM_BYTES + (p.n <= WX_SMEM_MAX ? (size_t)p.n * 4 : 0);
+        k_tile_middle<<<grid, THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap *>(ctx->tmA),
                                                          *reinterpret_cast<const CUtensorMap *>(ctx->tmC), p,
                                                          delta, tile_lo, tile_hi - tile_lo);
         launches++;

@@ -51,7 +51,8 @@ __device__ __forceinline__ double ld(const double *p, bool fresh) { return fresh
 // loads of split k+1 are issued before the arithmetic of split k.
 constexpr int PH = SB / 2;  // columns per lane
 
-__global__ void __launch_bounds__(DEP_THREADS, 3) k_sub_product(Problem p, int delta, int e, int tile_lo,
+template <int MINB>
+__global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product(Problem p, int delta, int e, int tile_lo,
                                                                 int ntiles) {
     const int n = p.n, S = p.S;
     const int cnt = sub_count(delta, e);
@@ -86,8 +87,15 @@ __global__ void __launch_bounds__(DEP_THREADS, 3) k_sub_product(Problem p, int d
         fC2 = false;  // C(s', t) in tile (J,J)
         partial = delta >= 2;
     }
-    if (hi1 < lo1 && hi2 < lo2) return;
-    if (m > S || s0 > n || t0 > n) return;  // sub-tiles past the last stage have no cells
+    if (hi1 < lo1 && hi2 < lo2) return;     // uniform over the warp
+    if (s0 > n || t0 > n) return;           // sub-tiles past the last stage have no cells (uniform)
+    // the shifts of both split ranges, staged per warp (no global load on the split loop's critical path)
+    __shared__ int wxs[DEP_THREADS / 32][2 * TB];
+    int *ws = wxs[threadIdx.x >> 5];
+    if (lo1 + lane <= hi1) ws[lane] = p.wx[lo1 + lane - 1];
+    if (lo2 + lane <= hi2) ws[TB + lane] = p.wx[lo2 + lane - 1];
+    __syncwarp();
+    if (m > S) return;
     const int64_t pitch = p.pitch;
     const int tl = t0 + jh;  // first column of this lane
     double acc[SB][PH];
@@ -110,7 +118,7 @@ __global__ void __launch_bounds__(DEP_THREADS, 3) k_sub_product(Problem p, int d
 #pragma unroll
             for (int u = 0; u < 2; u++) {
                 const int q = sp + u;
-                const int w = q <= hi ? p.wx[q - 1] : 0;
+                const int w = q <= hi ? ws[r * TB + (q - lo)] : 0;
                 const bool use = q <= hi && m >= w;
                 const double *ap = p.A + a_index(s0, q - 1) * pitch + m;           // A(s0+i, q-1)
                 const double *cp = p.C + cell_index(n, q, tl) * pitch + (m - w);  // C(q, tl+j)
@@ -714,6 +722,17 @@ inline int leaf_variant() {
     return v;
 }
 
+// k_sub_product occupancy: 3 CTAs/SM (<= 170 registers, no spill) or 4
+// (<= 128, small spill); ROTOR_PROD=3|4 for A/B runs.
+constexpr int PRODUCT_MINB_DEFAULT = 3;
+inline int product_minb() {
+    static const int v = [] {
+        const char *e = getenv("ROTOR_PROD");
+        return e ? atoi(e) : PRODUCT_MINB_DEFAULT;
+    }();
+    return v;
+}
+
 // Launch the dependent phase of tile diagonal delta; returns the launch count.
 // phase_id: running counter of leaf launches in this solve (flags zeroed at
 // the start of the fill, so phase ids >= 1 never match stale values).
@@ -741,7 +760,10 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
             has_product = !(cnt == 1 && a == NSB - 1 && g == 0);
         }
         if (has_product) {
-            k_sub_product<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
+            if (product_minb() == 4)
+                k_sub_product<4><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
+            else
+                k_sub_product<3><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
             launches++;
         }
         const int lb = ntiles * cnt * n_chunks;
