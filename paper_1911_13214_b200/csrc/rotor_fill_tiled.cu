@@ -33,9 +33,12 @@ namespace rotor {
 namespace tiled {
 
 constexpr int TB = 32;      // tile edge in stages
-constexpr int KC = 4;       // splits per pipeline stage
+constexpr int KC = 8;       // splits per pipeline stage
 constexpr int TM = 16;      // m values per CTA (middle kernel)
-constexpr int STAGES = 6;   // TMA pipeline depth (5 stages in flight while one is consumed)
+constexpr int STAGES = 3;   // TMA pipeline depth (2 stages in flight while one is consumed)
+// Ring geometry measured at config 4 (same 209 KB of shared memory): KC x STAGES
+// = 8 x 3: 268 ms per solve, 4 x 6: 282 ms, 2 x 12: 299 ms — fewer, larger
+// stages amortise the per-stage barrier wait / arrive / refill.
 constexpr int CONSUMERS = 512;  // 16 warps: two per scheduler slot more than 8 hide the DADD->DSETP->FSEL chain
 constexpr int THREADS = CONSUMERS;
 constexpr int RS = 4, RT = 8;            // register tile (s x t) per consumer thread (<= 128 registers)
@@ -51,6 +54,10 @@ constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * 8 + 2 * STA
 // The rest of the 227 KB holds a copy of wx (the producer's shift lookups stay
 // on chip: a global load there delays every refill by a memory round trip).
 constexpr int WX_SMEM_MAX = (int)((226 * 1024 - SMEM_BYTES) / 4);  // 1 KB kept for the static/system share
+constexpr size_t ring_bytes(int kc, int stages) {
+    return (size_t)stages * kc * TB * (TM + TMB) * 8 + 2 * stages * 8 + stages * kc * 4 + 64;
+}
+static_assert(ring_bytes(KC, STAGES) == SMEM_BYTES, "ring size");
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -118,9 +125,12 @@ constexpr int INT_MIN_COLS = 0;  // register-tile columns j >= RT - INT_MIN_COLS
 // 16 warps (thread = one m, a 4x8 (s,t) register tile); thread 0 also issues
 // the 2*KC TMA boxes of each stage (full/empty mbarrier ring).
 // ---------------------------------------------------------------------------
+template <int KC_, int STAGES_>
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC, Problem p,
                   int delta, int tile_lo, int n_tiles) {
+    constexpr int KC = KC_, STAGES = STAGES_;  // ring geometry (KC splits per stage)
+    constexpr int A_STAGE = KC * TB * TM, B_STAGE = KC * TB * TMB;
     extern __shared__ __align__(1024) double smem[];  // no static smem: the dynamic base is aligned
     double *As = smem;                     // [STAGES][KC][TB][TM]
     double *Bs = smem + STAGES * A_STAGE;  // [STAGES][KC][TB][TMB]
@@ -294,7 +304,7 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     static_assert(sizeof(CUtensorMap) <= sizeof(ctx->tmA), "tensor map storage");
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(k_tile_middle, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        if (cudaFuncSetAttribute(k_tile_middle<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) !=
                 cudaSuccess ||
             cudaFuncSetAttribute(k_sub_leaf_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LEAF_SMEM) !=
@@ -328,9 +338,9 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
         const int n_items = (tile_hi - tile_lo) * ((p.S + 1 + TM - 1) / TM);
         const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
         const size_t smem = SMEM_BYTES + (p.n <= WX_SMEM_MAX ? (size_t)p.n * 4 : 0);
-        k_tile_middle<<<grid, THREADS, smem, st>>>(*reinterpret_cast<const CUtensorMap *>(ctx->tmA),
-                                                         *reinterpret_cast<const CUtensorMap *>(ctx->tmC), p,
-                                                         delta, tile_lo, tile_hi - tile_lo);
+        const CUtensorMap &tmA = *reinterpret_cast<const CUtensorMap *>(ctx->tmA);
+        const CUtensorMap &tmC = *reinterpret_cast<const CUtensorMap *>(ctx->tmC);
+        k_tile_middle<KC, STAGES><<<grid, THREADS, smem, st>>>(tmA, tmC, p, delta, tile_lo, tile_hi - tile_lo);
         launches++;
     }
     return launches + launch_dependent(p, delta, tile_lo, tile_hi, st, p.flags, ctx->phase_id);
