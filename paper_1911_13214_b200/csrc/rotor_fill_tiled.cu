@@ -183,8 +183,10 @@ __global__ void __launch_bounds__(THREADS, 1)
             const int c0 = max(m0 - wxp[sp - 1], -kPad) + kPad;
             tma_load_2d(Bs + st * B_STAGE + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp, j0), &full[st]);
         }
-        // (an L2 prefetch of the next ring's boxes, cp.async.bulk.prefetch.tensor,
-        // measured slower: 204 vs 164 ms of middle time at config 4 — not used)
+        // (an L2 prefetch of later steps' boxes, cp.async.bulk.prefetch.tensor,
+        // measured slower: 1 or 2 steps ahead 296 vs 265 ms of fill, 6 steps
+        // ahead with the 4 x 6 ring 204 vs 164 ms of middle time — not used;
+        // so was a non-blocking "lazy" refill by the producer lane, 293 vs 288)
     };
 
     if (tid == 0) {
