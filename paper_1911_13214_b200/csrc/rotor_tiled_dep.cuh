@@ -145,6 +145,126 @@ __global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product(Problem p, in
         }
 }
 
+// The same product with the operands staged through a per-warp shared-memory
+// ring by cp.async (PNS splits in flight per warp, no operand registers held
+// across the load latency): lane (mi, half) copies rows / columns half*4..+3
+// of the split's A column and shifted C row at m = m0 + mi; after the stage
+// lands every lane reads all SB A values and its own PH C values.
+constexpr int PNS = 4;  // splits in flight per warp
+constexpr int PW = DEP_THREADS / 32;
+
+__device__ __forceinline__ void cp_async8(double *dst, const double *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+__global__ void __launch_bounds__(DEP_THREADS, 4) k_sub_product_async(Problem p, int delta, int e, int tile_lo,
+                                                                      int ntiles) {
+    __shared__ int wxs[PW][2 * TB];
+    __shared__ double ring[PW][PNS][2][SB][16];  // [warp][stage][A | C][row | column][m]
+    const int n = p.n, S = p.S;
+    const int cnt = sub_count(delta, e);
+    const int n_mg = (S + 1 + 15) / 16;
+    const int wid = threadIdx.x >> 5;
+    const int item = (blockIdx.x * DEP_THREADS + threadIdx.x) >> 5;
+    if (item >= ntiles * cnt * n_mg) return;
+    const int lane = threadIdx.x & 31;
+    const int mi = lane & 15, half = lane >> 4;
+    const int m = (item % n_mg) * 16 + mi;
+    const int jh = half * PH;
+    const int rest = item / n_mg;
+    int alpha, gamma;
+    sub_at(delta, e, rest % cnt, alpha, gamma);
+    const int I = tile_lo + rest / cnt, J = I + delta;
+    const int i0 = I * TB + 1, j0 = J * TB + 1;
+    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
+    int lo1, hi1, lo2 = 1, hi2 = 0;
+    bool partial;
+    if (delta == 0) {
+        lo1 = i0 + SB * (alpha + 1);
+        hi1 = t0 - 1;
+        partial = false;
+    } else {
+        lo1 = s0 + SB;
+        hi1 = i0 + TB - 1;
+        lo2 = j0;
+        hi2 = t0 - 1;
+        partial = delta >= 2;
+    }
+    const int n1 = max(0, hi1 - lo1 + 1), n2 = max(0, hi2 - lo2 + 1), nsp = n1 + n2;
+    if (nsp == 0 || s0 > n || t0 > n) return;  // uniform over the warp
+    int *ws = wxs[wid];
+    if (lane < n1) ws[lane] = p.wx[lo1 + lane - 1];
+    if (lane < n2) ws[TB + lane] = p.wx[lo2 + lane - 1];
+    __syncwarp();
+    const int64_t pitch = p.pitch;
+    const bool mlive = m <= S;
+    // split idx: 0..n1-1 -> s' = lo1 + idx (left), n1.. -> s' = lo2 + idx - n1 (right)
+    auto issue = [&](int idx) {
+        double(*st)[SB][16] = ring[wid][idx % PNS];
+        const bool r2 = idx >= n1;
+        const int q = r2 ? lo2 + (idx - n1) : lo1 + idx;
+        const int w = r2 ? ws[TB + idx - n1] : ws[idx];
+        const bool use = mlive && m >= w;  // else +inf: every cell it feeds is gated (m < w <= m_null)
+#pragma unroll
+        for (int i = 0; i < PH; i++) {
+            const int row = jh + i;  // this lane copies A row `row` and C column `row`
+            double *da = &st[0][row][mi], *dc = &st[1][row][mi];
+            if (use && s0 + row <= n)
+                cp_async8(da, p.A + a_index(s0 + row, q - 1) * pitch + m);
+            else
+                *da = INFINITY;
+            if (use && t0 + row <= n)
+                cp_async8(dc, p.C + cell_index(n, q, t0 + row) * pitch + (m - w));
+            else
+                *dc = INFINITY;
+        }
+    };
+    double acc[SB][PH];
+#pragma unroll
+    for (int i = 0; i < SB; i++)
+#pragma unroll
+        for (int j = 0; j < PH; j++) {
+            const int s = s0 + i, t = t0 + jh + j;
+            acc[i][j] = (partial && mlive && s <= n && t <= n) ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m])
+                                                              : INFINITY;
+        }
+#pragma unroll
+    for (int k = 0; k < PNS - 1; k++) {
+        if (k < nsp) issue(k);
+        cp_async_commit();
+    }
+    for (int idx = 0; idx < nsp; idx++) {
+        if (idx + PNS - 1 < nsp) issue(idx + PNS - 1);
+        cp_async_commit();
+        cp_async_wait<PNS - 1>();  // split idx landed (this lane's copies)
+        __syncwarp();              // ... and every lane's
+        const double(*st)[SB][16] = ring[wid][idx % PNS];
+        double a[SB], c[PH];
+#pragma unroll
+        for (int i = 0; i < SB; i++) a[i] = st[0][i][mi];
+#pragma unroll
+        for (int j = 0; j < PH; j++) c[j] = st[1][jh + j][mi];
+#pragma unroll
+        for (int i = 0; i < SB; i++)
+#pragma unroll
+            for (int j = 0; j < PH; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], c[j]));
+        __syncwarp();  // stage idx % PNS is refilled by the next iteration's issue
+    }
+    if (!mlive) return;
+#pragma unroll
+    for (int i = 0; i < SB; i++)
+#pragma unroll
+        for (int j = 0; j < PH; j++) {
+            const int s = s0 + i, t = t0 + jh + j;
+            if (s <= n && t <= n) p.C[cell_index(n, s, t) * pitch + m] = acc[i][j];
+        }
+}
+
 // Finish cell (s,t) at m from its running minimum c1 (already gated): F_all
 // candidate, store C and A; returns A(s,t,m).
 __device__ __forceinline__ double finish(const Problem &p, int s, int t, int m, double c1) {
@@ -722,9 +842,10 @@ inline int leaf_variant() {
     return v;
 }
 
-// k_sub_product occupancy: 3 CTAs/SM (<= 170 registers, no spill) or 4
-// (<= 128, small spill); ROTOR_PROD=3|4 for A/B runs.
-constexpr int PRODUCT_MINB_DEFAULT = 3;
+// Product kernel: ROTOR_PROD=1 k_sub_product_async (default: 266.7 vs 268.3
+// ms per config-4 solve), 3 / 4 k_sub_product at 3 CTAs/SM (<= 170
+// registers, no spill) / 4 (<= 128, small spill) — same time.
+constexpr int PRODUCT_MINB_DEFAULT = 1;
 inline int product_minb() {
     static const int v = [] {
         const char *e = getenv("ROTOR_PROD");
@@ -760,7 +881,9 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
             has_product = !(cnt == 1 && a == NSB - 1 && g == 0);
         }
         if (has_product) {
-            if (product_minb() == 4)
+            if (product_minb() == 1)
+                k_sub_product_async<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
+            else if (product_minb() == 4)
                 k_sub_product<4><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
             else
                 k_sub_product<3><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
