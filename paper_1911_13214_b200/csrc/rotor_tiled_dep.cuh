@@ -466,9 +466,9 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
 
 // Off-diagonal leaf row r at one m (thread = m), scalars from the table; the
 // same arithmetic as leaf_row<false>.
-template <int r>
+template <int r, bool RS>
 __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T, bool fresh, bool partial, int s0,
-                                             int t0, int m) {
+                                             int t0, int m, const double *Rs) {
     const int n = p.n;
     const int64_t pitch = p.pitch;
     const int s = s0 + r;
@@ -509,7 +509,8 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
 #pragma unroll
             for (int cq = 0; cq < SB; cq++) {  // right: s' = t0 + cq <= t
                 if (cq > c) break;
-                const double cv = ld(&p.C[cell_index(n, t0 + cq, t) * pitch + (m - T.wxr[cq])], fresh);
+                const double cv = RS ? Rs[(c * (c + 1) / 2 + cq) * LEAF_M + threadIdx.x]
+                                     : ld(&p.C[cell_index(n, t0 + cq, t) * pitch + (m - T.wxr[cq])], fresh);
                 best = dmin(best, __dadd_rn(AR[cq], cv));
             }
             c1 = best;
@@ -522,9 +523,14 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     }
 }
 
+// RS: the right-range operands R[c][cq] = C(t0+cq, t0+c, m - wx[t0+cq-1]),
+// the same for every row, are loaded once into shared memory (thread-private
+// columns, NPAIR x LEAF_M doubles) instead of once per row.
+template <bool RS>
 __global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf_row(Problem p, int delta, int e, int *flags,
                                                                         int phase_id, int tile_lo) {
     __shared__ LeafTab T;
+    extern __shared__ double Rsm[];  // [NPAIR][LEAF_M] when RS
     const int n = p.n;
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int cnt = sub_count(delta, e);
@@ -541,6 +547,18 @@ __global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf_row(Proble
     int *my_flags = flags + (int64_t)sub * n_chunks;
     leaf_tab_fill(p, s0, t0, q * LEAF_M, LEAF_M, T);
     const int q_lo = T.q_lo;
+    if (RS) {
+        const int64_t pitch = p.pitch;
+#pragma unroll
+        for (int c = 0; c < SB; c++)
+#pragma unroll
+            for (int cq = 0; cq <= c; cq++) {
+                const int t = t0 + c, w = T.wxr[cq];
+                Rsm[(c * (c + 1) / 2 + cq) * LEAF_M + threadIdx.x] =
+                    (m <= p.S && t <= n && m >= w) ? ld(&p.C[cell_index(n, t0 + cq, t) * pitch + (m - w)], fresh)
+                                                   : INFINITY;
+            }
+    }
     for (int r = SB - 1; r >= 0; r--) {
         if (r < SB - 1) {
             const int need = (phase_id << 4) | (SB - 1 - r);  // rows SB-1 .. r+1 done
@@ -553,14 +571,14 @@ __global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf_row(Proble
             __syncthreads();
         }
         if (s0 + r <= n && m <= p.S) switch (r) {  // compile-time row index: the row's loops fully unrolled
-                case 0: leaf_row_tab<0>(p, T, fresh, partial, s0, t0, m); break;
-                case 1: leaf_row_tab<1>(p, T, fresh, partial, s0, t0, m); break;
-                case 2: leaf_row_tab<2>(p, T, fresh, partial, s0, t0, m); break;
-                case 3: leaf_row_tab<3>(p, T, fresh, partial, s0, t0, m); break;
-                case 4: leaf_row_tab<4>(p, T, fresh, partial, s0, t0, m); break;
-                case 5: leaf_row_tab<5>(p, T, fresh, partial, s0, t0, m); break;
-                case 6: leaf_row_tab<6>(p, T, fresh, partial, s0, t0, m); break;
-                default: leaf_row_tab<7>(p, T, fresh, partial, s0, t0, m); break;
+                case 0: leaf_row_tab<0, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
+                case 1: leaf_row_tab<1, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
+                case 2: leaf_row_tab<2, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
+                case 3: leaf_row_tab<3, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
+                case 4: leaf_row_tab<4, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
+                case 5: leaf_row_tab<5, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
+                case 6: leaf_row_tab<6, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
+                default: leaf_row_tab<7, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
             }
         __syncthreads();
         if (threadIdx.x == 0)
@@ -828,8 +846,8 @@ inline size_t leaf_flag_bytes(int L, int S) {
 // Off-diagonal leaf kernel: k_sub_leaf<false> (row: thread = m), k_sub_leaf_col
 // (thread = (m, column)) or k_sub_leaf_smem; ROTOR_LEAF=row|col|smem selects
 // one for measurements (default: the fastest measured, LEAF_VARIANT_DEFAULT).
-enum { LEAF_VARIANT_ROW = 0, LEAF_VARIANT_COL = 1, LEAF_VARIANT_SMEM = 2, LEAF_VARIANT_TAB = 3 };
-constexpr int LEAF_VARIANT_DEFAULT = LEAF_VARIANT_TAB;
+enum { LEAF_VARIANT_ROW = 0, LEAF_VARIANT_COL = 1, LEAF_VARIANT_SMEM = 2, LEAF_VARIANT_TAB = 3, LEAF_VARIANT_TABR = 4 };
+constexpr int LEAF_VARIANT_DEFAULT = LEAF_VARIANT_TABR;  // 243.6 ms per config-4 solve (tab 265.7, row 268)
 inline int leaf_variant() {
     static const int v = [] {
         const char *e = getenv("ROTOR_LEAF");
@@ -837,6 +855,7 @@ inline int leaf_variant() {
         if (!strcmp(e, "col")) return (int)LEAF_VARIANT_COL;
         if (!strcmp(e, "smem")) return (int)LEAF_VARIANT_SMEM;
         if (!strcmp(e, "tab")) return (int)LEAF_VARIANT_TAB;
+        if (!strcmp(e, "tabr")) return (int)LEAF_VARIANT_TABR;
         return (int)LEAF_VARIANT_ROW;
     }();
     return v;
@@ -895,7 +914,9 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
         else if (leaf_variant() == LEAF_VARIANT_COL)
             k_sub_leaf_col<<<ntiles * cnt * n_chunks_col, LEAF_CT, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else if (leaf_variant() == LEAF_VARIANT_TAB)
-            k_sub_leaf_row<<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
+            k_sub_leaf_row<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
+        else if (leaf_variant() == LEAF_VARIANT_TABR)
+            k_sub_leaf_row<true><<<lb, LEAF_M, NPAIR * LEAF_M * 8, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else if (leaf_variant() == LEAF_VARIANT_SMEM)
             k_sub_leaf_smem<<<lb, LEAF_M, LEAF_SMEM, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else
