@@ -527,7 +527,7 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
 // the same for every row, are loaded once into shared memory (thread-private
 // columns, NPAIR x LEAF_M doubles) instead of once per row.
 template <bool RS>
-__global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf_row(Problem p, int delta, int e, int *flags,
+__global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_row(Problem p, int delta, int e, int *flags,
                                                                         int phase_id, int tile_lo) {
     __shared__ LeafTab T;
     extern __shared__ double Rsm[];  // [NPAIR][LEAF_M] when RS
