@@ -147,6 +147,17 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def ncu_step_traffic(key: str):
+    """DRAM read+write bytes of all launches of one solve, from the committed ncu launch list summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            ent = json.load(f).get(key)
+        return None if ent is None else ent.get("dram_bytes_per_step")
+    except Exception:
+        return None
+
+
 def ncu_traffic(kernel_tag: str):
     """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -486,8 +497,10 @@ def run_ours(args):
         peak = 148 * (64.0 / 3.0) * clk_mhz * 1e6 / 1e9  # Gtransitions/s
         achieved = tr / (fill_avg_ms / 1e3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gtransitions/s",
-                    "frac": achieved / peak, "traffic": ncu_traffic("k_tile_middle"),
-                    "kernel": "tiled fill (k_tile_middle + k_tile_dep, all tile diagonals)",
+                    "frac": achieved / peak, "traffic": ncu_step_traffic("tiled_solve"),
+                    "traffic_scope": "DRAM read+write bytes of every launch of one solve (ncu launch list, "
+                                     "profiles/ncu_summary.json tiled_solve)",
+                    "kernel": "tiled fill (k_tile_middle + k_sub_product + k_sub_leaf, all tile diagonals)",
                     "peak_model": "148 SMs x sm_max_mhz x 21.33 transitions/clk/SM (fp64 pipe: DADD 64 "
                                   "lanes/clk + DSETP 32 lanes/clk per SM, measured scripts/microbench_minplus.cu)",
                     "launches_per_step": fill_launches, "fill_ms_per_step": fill_avg_ms,

@@ -210,16 +210,19 @@ __global__ void __launch_bounds__(DEP_THREADS, 4) k_sub_product_async(Problem p,
         const int q = r2 ? lo2 + (idx - n1) : lo1 + idx;
         const int w = r2 ? ws[TB + idx - n1] : ws[idx];
         const bool use = mlive && m >= w;  // else +inf: every cell it feeds is gated (m < w <= m_null)
+        // rows s0+jh.. of A column q-1 and cells (q, t0+jh..) are consecutive rows of their tables
+        const double *ga = p.A + a_index(s0 + jh, q - 1) * pitch + m;
+        const double *gc = p.C + cell_index(n, q, t0 + jh) * pitch + (m - w);
 #pragma unroll
         for (int i = 0; i < PH; i++) {
             const int row = jh + i;  // this lane copies A row `row` and C column `row`
             double *da = &st[0][row][mi], *dc = &st[1][row][mi];
             if (use && s0 + row <= n)
-                cp_async8(da, p.A + a_index(s0 + row, q - 1) * pitch + m);
+                cp_async8(da, ga + i * pitch);
             else
                 *da = INFINITY;
             if (use && t0 + row <= n)
-                cp_async8(dc, p.C + cell_index(n, q, t0 + row) * pitch + (m - w));
+                cp_async8(dc, gc + i * pitch);
             else
                 *dc = INFINITY;
         }

@@ -1,6 +1,7 @@
 """Summarise ncu outputs into profiles/.
 
-  python scripts/ncu_summary.py launches <launches.csv>          per-kernel share of one step
+  python scripts/ncu_summary.py launches <launches.csv> [key]    per-kernel share of one step
+                                                                 (key: record the totals in the json)
   python scripts/ncu_summary.py full <prof.ncu-rep> [tag]         key metrics of the full capture
 Writes nothing by itself; prints markdown (redirect into profiles/).  `full`
 also updates profiles/ncu_summary.json (dram bytes per launch by kernel tag),
@@ -23,24 +24,47 @@ def _csv_rows(text):
     return list(csv.reader(io.StringIO("\n".join(lines[start:]))))
 
 
-def launches(path):
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
+def launches(path, record=None):
+    """Per-kernel time (and DRAM bytes when the list carries dram__bytes_*) of one step.
+    With `record`, the per-step totals go to profiles/ncu_summary.json[record]."""
     rows = _csv_rows(open(path).read())
     h = rows[0]
     ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value")
+    ui = h.index("Metric Unit") if "Metric Unit" in h else None
     tot = collections.defaultdict(float)
+    dram = collections.defaultdict(float)
     cnt = collections.Counter()
     for r in rows[1:]:
-        if r[mi] != "gpu__time_duration.sum":
-            continue
         k = r[ki].split("(")[0]
-        tot[k] += float(r[vi].replace(",", ""))
-        cnt[k] += 1
+        v = float(r[vi].replace(",", ""))
+        if r[mi] == "gpu__time_duration.sum":
+            tot[k] += v
+            cnt[k] += 1
+        elif r[mi] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            dram[k] += v * (UNIT.get(r[ui], 1) if ui is not None else 1)
     T = sum(tot.values())
-    print("| kernel | launches | total ms (ncu, serialised, cold) | share |")
-    print("|---|---|---|---|")
+    has_dram = bool(dram)
+    print("| kernel | launches | total ms (ncu, serialised, cold) | share |" + (" DRAM GB |" if has_dram else ""))
+    print("|---|---|---|---|" + ("---|" if has_dram else ""))
     for k, v in sorted(tot.items(), key=lambda kv: -kv[1]):
-        print(f"| {k} | {cnt[k]} | {v / 1e6:.2f} | {100 * v / T:.2f}% |")
-    print(f"| total | {sum(cnt.values())} | {T / 1e6:.2f} | 100% |")
+        print(f"| {k} | {cnt[k]} | {v / 1e6:.2f} | {100 * v / T:.2f}% |" + (f" {dram[k] / 1e9:.2f} |" if has_dram else ""))
+    D = sum(dram.values())
+    print(f"| total | {sum(cnt.values())} | {T / 1e6:.2f} | 100% |" + (f" {D / 1e9:.2f} |" if has_dram else ""))
+    if record:
+        js_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+        try:
+            js = json.load(open(js_path))
+        except Exception:
+            js = {}
+        js[record] = {"dram_bytes_per_step": D if has_dram else None, "ms_per_step": T / 1e6,
+                      "launches": sum(cnt.values()), "source": os.path.relpath(path, ROOT),
+                      "per_kernel": {k: {"launches": cnt[k], "ms": tot[k] / 1e6, "dram_bytes": dram.get(k)}
+                                     for k in tot}}
+        with open(js_path, "w") as f:
+            json.dump(js, f, indent=1)
 
 
 KEYS = [
@@ -94,6 +118,6 @@ def full(path, tag=None):
 
 if __name__ == "__main__":
     if sys.argv[1] == "launches":
-        launches(sys.argv[2])
+        launches(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
     else:
         full(sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)
