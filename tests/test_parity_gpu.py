@@ -156,6 +156,21 @@ def test_tiled_block_boundaries(R, oracle_mod, L):
     check_against_oracle(R, O, ch2, 24, 24, kernel="tiled")
 
 
+@pytest.mark.parametrize("S", [15, 16, 17, 127, 128, 129, 255, 257, 520])
+def test_tiled_m_chunk_boundaries(R, oracle_mod, S):
+    """S + 1 around the m-chunks of the tiled kernels (16 m per middle item and
+    sub-product warp, 128 m per leaf CTA, 32 / 128 look-back chunks), with
+    shifts from a fraction of a chunk to several chunks (big sizes, tight and
+    loose limits): full tables bit-exact, both modes."""
+    O = oracle_mod
+    rng = G.SplitMix64(5000 + S)
+    ch = G.random_chain(rng, 70, real_times=True, big=True)
+    for f in (0.12, 0.35):
+        M = max(1, int(sum(int(x) for x in ch.wbx) * f))
+        check_against_oracle(R, O, ch, M, S, kernel="tiled")
+    check_against_oracle(R, O, ch, M, S, kernel="tiled", restricted=True)
+
+
 def test_device_resident_path(R, oracle_mod):
     import torch
 
