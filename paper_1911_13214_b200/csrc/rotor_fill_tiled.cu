@@ -186,7 +186,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         // (an L2 prefetch of later steps' boxes, cp.async.bulk.prefetch.tensor,
         // measured slower: 1 or 2 steps ahead 296 vs 265 ms of fill, 6 steps
         // ahead with the 4 x 6 ring 204 vs 164 ms of middle time — not used;
-        // so was a non-blocking "lazy" refill by the producer lane, 293 vs 288)
+        // so was a non-blocking "lazy" refill by the producer lane, 293 vs 288,
+        // and prefetch.global.L2 of the boxes 4-7 steps ahead spread over all
+        // 512 threads, 247-251 vs 234 ms of fill)
     };
 
     if (tid == 0) {
