@@ -162,7 +162,7 @@ int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_ch
  * ------------------------------------------------------------------------- */
 typedef struct rotor_shard rotor_shard;
 int32_t rotor_tile_blocks(int32_t L);                 /* ceil((L+1)/32) */
-int rotor_tile_bytes(int32_t slots, uint64_t *bytes); /* packed bytes per tile (C and A rows, all m) */
+int rotor_tile_bytes(int32_t slots, uint64_t *bytes); /* packed bytes per tile (its C rows, all m) */
 /* discretise + limits + leaf diagonal + setup; d_chain and the workspace as in
  * rotor_solve_device (options: kernel forced to TILED).  *out: new handle. */
 int rotor_sharded_begin(const rotor_chain *d_chain, int32_t L, uint64_t mem_limit, int32_t slots,
@@ -171,8 +171,10 @@ int rotor_sharded_begin(const rotor_chain *d_chain, int32_t L, uint64_t mem_limi
 /* middle + dependent phase of the tiles I in [tile_lo, tile_hi) of diagonal delta
  * (0 <= tile_lo <= tile_hi <= rotor_tile_blocks(L) - delta) */
 int rotor_sharded_step(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t tile_hi, void *stream);
-/* copy those tiles' C and A rows to (unpack = 0) or from (unpack = 1) d_buf:
- * layout [tile][C|A][32 s][32 t][S+1] fp64; buf_bytes >= count * rotor_tile_bytes */
+/* copy those tiles' C rows to (unpack = 0) or from (unpack = 1) d_buf, layout
+ * [tile][32 s][32 t][S+1] fp64, buf_bytes >= count * rotor_tile_bytes; unpack
+ * also rebuilds the A rows, A(s,t,m) = fl(fl(P[t] - P[s-1]) + C(s,t,m)) (the
+ * fill's own association, Q12: bit-identical), so only C travels */
 int rotor_sharded_pack(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t tile_hi, void *d_buf,
                        uint64_t buf_bytes, int32_t unpack, void *stream);
 /* Algorithm 2 on the completed table; outputs as in rotor_solve_device.  Also

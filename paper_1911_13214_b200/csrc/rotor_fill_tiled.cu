@@ -365,29 +365,38 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st) {
 // one tile diagonal into a contiguous buffer [tile][C|A][TB s][TB t][S+1].
 // Cells that do not exist (s > t, t > n; A at t = n) are skipped both ways.
 // ---------------------------------------------------------------------------
-size_t tiled_tile_bytes(int S) { return (size_t)2 * tiled::TB * tiled::TB * (S + 1) * sizeof(double); }
+// One finished tile travels as its C rows only (TB x TB x (S+1) fp64): the
+// receiver rebuilds A(s,t,m) = fl(fl(P[t] - P[s-1]) + C(s,t,m)) with the same
+// association as the producing kernels (Q12), so its A rows are bit-identical
+// and the exchange volume is half of sending both tables.
+size_t tiled_tile_bytes(int S) { return (size_t)tiled::TB * tiled::TB * (S + 1) * sizeof(double); }
 
 __global__ void k_tile_pack(Problem p, int delta, int tile_lo, double *buf, int unpack) {
     using namespace tiled;
     const int n = p.n, W = p.S + 1;
-    const int tile = blockIdx.z, a = blockIdx.y / TB, c = blockIdx.y % TB, which = blockIdx.x & 1;
+    const int tile = blockIdx.z, a = blockIdx.y / TB, c = blockIdx.y % TB;
     const int I = tile_lo + tile, J = I + delta;
     const int s = I * TB + 1 + a, t = J * TB + 1 + c;
-    if (s > n || t > n || s > t || (which == 1 && t == n)) return;
-    const double *row_src = which == 0 ? p.C + cell_index(n, s, t) * p.pitch : p.A + a_index(s, t) * p.pitch;
-    double *packed = buf + ((((int64_t)tile * 2 + which) * TB + a) * TB + c) * W;
-    double *row = const_cast<double *>(row_src);
-    for (int m = (blockIdx.x >> 1) * blockDim.x + threadIdx.x; m < W; m += (gridDim.x >> 1) * blockDim.x) {
-        if (unpack)
-            row[m] = packed[m];
-        else
-            packed[m] = row[m];
+    if (s > n || t > n || s > t) return;
+    double *crow = p.C + cell_index(n, s, t) * p.pitch;
+    double *packed = buf + (((int64_t)tile * TB + a) * TB + c) * W;
+    const bool has_a = t < n;  // A(s, n) is never an operand
+    double *arow = has_a ? p.A + a_index(s, t) * p.pitch : nullptr;
+    const double u = has_a ? __dadd_rn(p.P[t], -p.P[s - 1]) : 0.0;
+    for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < W; m += gridDim.x * blockDim.x) {
+        if (unpack) {
+            const double v = packed[m];
+            crow[m] = v;
+            if (has_a) arow[m] = __dadd_rn(u, v);
+        } else {
+            packed[m] = crow[m];
+        }
     }
 }
 
 int tiled_pack(const Problem &p, int delta, int tile_lo, int tile_hi, double *buf, int unpack, cudaStream_t st) {
     if (tile_hi <= tile_lo) return 0;
-    dim3 grid(2 * 4, tiled::TB * tiled::TB, tile_hi - tile_lo);
+    dim3 grid(4, tiled::TB * tiled::TB, tile_hi - tile_lo);
     k_tile_pack<<<grid, 256, 0, st>>>(p, delta, tile_lo, buf, unpack);
     return 1;
 }
