@@ -502,6 +502,7 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
                    ? __dadd_rn(T.w[r], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - T.wbx[r])]))
                    : INFINITY;
     }
+    if (RS) cp_async_wait<0>();  // this thread's right-range operands are in shared memory
 #pragma unroll
     for (int c = 0; c < SB; c++) {
         const int t = t0 + c;
@@ -558,10 +559,13 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
 #pragma unroll
             for (int cq = 0; cq <= c; cq++) {
                 const int t = t0 + c, w = T.wxr[cq];
-                Rsm[(c * (c + 1) / 2 + cq) * LEAF_M + threadIdx.x] =
-                    (m <= p.S && t <= n && m >= w) ? ld(&p.C[cell_index(n, t0 + cq, t) * pitch + (m - w)], fresh)
-                                                   : INFINITY;
+                double *dst = &Rsm[(c * (c + 1) / 2 + cq) * LEAF_M + threadIdx.x];
+                if (m <= p.S && t <= n && m >= w)  // lands while the first row's pass 1 runs
+                    cp_async8(dst, &p.C[cell_index(n, t0 + cq, t) * pitch + (m - w)]);
+                else
+                    *dst = INFINITY;
             }
+        cp_async_commit();
     }
     for (int r = SB - 1; r >= 0; r--) {
         if (r < SB - 1) {
