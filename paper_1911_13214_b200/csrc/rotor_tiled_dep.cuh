@@ -469,26 +469,35 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
 
 // Off-diagonal leaf row r at one m (thread = m), scalars from the table; the
 // same arithmetic as leaf_row<false>.
-template <int r, bool RS>
+template <int r, bool RS, class Wait>
 __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T, bool fresh, bool partial, int s0,
-                                             int t0, int m, const double *Rs) {
+                                             int t0, int m, bool live, const double *Rs, Wait wait) {
     const int n = p.n;
     const int64_t pitch = p.pitch;
     const int s = s0 + r;
+    // operands written by earlier launches first — their loads are in flight
+    // during the look-back wait: A(s, ·) of the left splits, A(s, t0-1), and
+    // the partial minimum of the row's cells
     double AL[SB - 1];  // AL[k] = A(s, s + k): left split s' = s + k + 1 <= ea
 #pragma unroll
-    for (int k = 0; k < SB - 1; k++) AL[k] = (k < SB - 1 - r) ? ld(&p.A[a_index(s, s + k) * pitch + m], fresh) : INFINITY;
+    for (int k = 0; k < SB - 1; k++)
+        AL[k] = (live && k < SB - 1 - r) ? ld(&p.A[a_index(s, s + k) * pitch + m], fresh) : INFINITY;
     double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
-    AR[0] = __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]);
+    AR[0] = live ? __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]) : INFINITY;
     double B[SB], F[SB];
     bool gate[SB];
 #pragma unroll
     for (int c = 0; c < SB; c++) {
+        gate[c] = live && m >= T.mnull[r][c];  // INT_MAX past the last stage
+        B[c] = (gate[c] && partial) ? __ldcg(&p.C[cell_index(n, s, t0 + c) * pitch + m]) : INFINITY;
+    }
+    wait();  // the rows below are complete at every m this row reads (flags + barrier)
+    if (!live) return;
+#pragma unroll
+    for (int c = 0; c < SB; c++) {
         const int t = t0 + c;
-        gate[c] = m >= T.mnull[r][c];  // INT_MAX past the last stage
-        double best = INFINITY;
+        double best = B[c];
         if (gate[c]) {
-            best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
 #pragma unroll
             for (int k = 0; k < SB - 1; k++) {  // left: C of the rows below in this sub-tile
                 if (k >= SB - 1 - r) break;
@@ -568,7 +577,8 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
         cp_async_commit();
     }
     for (int r = SB - 1; r >= 0; r--) {
-        if (r < SB - 1) {
+        auto wait = [&]() {  // uniform over the CTA (every thread calls it once per row)
+            if (r == SB - 1) return;
             const int need = (phase_id << 4) | (SB - 1 - r);  // rows SB-1 .. r+1 done
             for (int qq = q_lo + (int)threadIdx.x; qq < q; qq += LEAF_M) {
                 int v;
@@ -577,17 +587,22 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
                 } while (v < need);
             }
             __syncthreads();
-        }
-        if (s0 + r <= n && m <= p.S) switch (r) {  // compile-time row index: the row's loops fully unrolled
-                case 0: leaf_row_tab<0, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
-                case 1: leaf_row_tab<1, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
-                case 2: leaf_row_tab<2, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
-                case 3: leaf_row_tab<3, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
-                case 4: leaf_row_tab<4, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
-                case 5: leaf_row_tab<5, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
-                case 6: leaf_row_tab<6, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
-                default: leaf_row_tab<7, RS>(p, T, fresh, partial, s0, t0, m, Rsm); break;
+        };
+        const bool live = m <= p.S;
+        if (s0 + r > n) {  // no such row (uniform)
+            wait();
+        } else {
+            switch (r) {  // compile-time row index: the row's loops fully unrolled
+                case 0: leaf_row_tab<0, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
+                case 1: leaf_row_tab<1, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
+                case 2: leaf_row_tab<2, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
+                case 3: leaf_row_tab<3, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
+                case 4: leaf_row_tab<4, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
+                case 5: leaf_row_tab<5, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
+                case 6: leaf_row_tab<6, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
+                default: leaf_row_tab<7, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
             }
+        }
         __syncthreads();
         if (threadIdx.x == 0)
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(my_flags + q), "r"((phase_id << 4) | (SB - r))
