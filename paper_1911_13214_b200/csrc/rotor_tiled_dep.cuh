@@ -536,7 +536,9 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     }
 }
 
-// (CTA width measured: 64 m 247.1, 128 m 238.9, 256 m 239.7 ms per solve.)
+// (CTA width measured: 64 m 247.1, 128 m 238.9, 256 m 239.7 ms per solve; one
+// runtime-row body instead of 8 unrolled row copies (17 K instructions, ncu
+// shows instruction-fetch stalls) measured slower: 238.1 vs 228.8.)
 // RS: the right-range operands R[c][cq] = C(t0+cq, t0+c, m - wx[t0+cq-1]),
 // the same for every row, are loaded once into shared memory (thread-private
 // columns, NPAIR x LEAF_M doubles) instead of once per row.
