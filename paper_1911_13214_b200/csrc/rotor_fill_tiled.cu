@@ -309,10 +309,7 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(k_tile_middle<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(k_sub_leaf_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LEAF_SMEM) !=
-                cudaSuccess)
+                                 (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess)
             return -1;
         attr = true;
     }

@@ -394,6 +394,7 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
 // has done the rows below.  CTAs of lower chunks have lower blockIdx and never
 // wait on higher ones, so the chain always progresses (decoupled look-back).
 constexpr int LEAF_M = 128;
+constexpr int NPAIR = SB * (SB + 1) / 2;  // right-range (column, split) pairs of a sub-tile row
 constexpr int LEAF_MIN_BLOCKS = 8;  // 32 warps/SM for the latency-bound leaf (<= 64 registers)
 
 template <bool DIAG>
@@ -612,273 +613,28 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
     }
 }
 
-__device__ __forceinline__ void leaf_wait(const int *my_flags, int q, int need) {
-    for (int qq = threadIdx.x; qq < q; qq += LEAF_M) {
-        int v;
-        do {
-            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(my_flags + qq) : "memory");
-        } while (v < need);
-    }
-}
-
-__device__ __forceinline__ void leaf_publish(int *flag, int value) {
-    if (threadIdx.x == 0) asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(value) : "memory");
-}
-
-// Off-diagonal leaf with its operands in shared memory:
-//   RS_[pair][x]   right-range C(s', t, m0+x - wx[s'-1]), s' <= t in the column
-//                  sub-block (36 pairs): the same for all 8 rows, staged once;
-//   CS_[r][c][x]   this CTA's own results C(s0+r, t0+c, m0+x), read by the
-//                  rows above at m - shift >= m0 (lower m: another chunk ->
-//                  global, behind the look-back flags).
-// Measured slower than the register leaf (147 vs 119 ms at config 4: the
-// chunk-boundary lanes fall back to serialized global loads and 102 KB of
-// shared memory leaves 8 warps/SM), so it is not launched by default.
-constexpr bool LEAF_USE_SMEM = false;
-constexpr int NPAIR = SB * (SB + 1) / 2;
-constexpr size_t LEAF_SMEM = (size_t)(NPAIR + SB * SB) * LEAF_M * 8;
-
-__global__ void __launch_bounds__(LEAF_M) k_sub_leaf_smem(Problem p, int delta, int e, int *flags, int phase_id,
-                                                          int tile_lo) {
-    extern __shared__ double lsm[];
-    double *RS_ = lsm;                   // [NPAIR][LEAF_M]
-    double *CS_ = lsm + NPAIR * LEAF_M;  // [SB][SB][LEAF_M]
-    const int n = p.n, S = p.S;
-    const int64_t pitch = p.pitch;
-    const int n_chunks = (S + 1 + LEAF_M - 1) / LEAF_M;
-    const int cnt = sub_count(delta, e);
-    const int q = blockIdx.x % n_chunks;
-    const int sub = blockIdx.x / n_chunks;
-    int alpha, gamma;
-    sub_at(delta, e, sub % cnt, alpha, gamma);
-    const int I = tile_lo + sub / cnt, J = I + delta;
-    const int i0 = I * TB + 1, j0 = J * TB + 1;
-    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
-    const int ea = s0 + SB - 1;
-    const int m0 = q * LEAF_M, tid = threadIdx.x, m = m0 + tid;
-    int *my_flags = flags + (int64_t)sub * n_chunks;
-    const bool live = s0 <= n && t0 <= n && m <= S;
-    const bool fresh = (delta == 0);  // right C and left A belong to this tile diagonal when delta = 0
-    const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
-
-    // stage the right-range operands (written by earlier launches): 36 independent loads
-    if (live) {
-#pragma unroll
-        for (int c = 0; c < SB; c++) {
-#pragma unroll
-            for (int cq = 0; cq <= c; cq++) {
-                const int t = t0 + c, sp = t0 + cq;
-                const int w = p.wx[sp - 1];
-                RS_[(c * (c + 1) / 2 + cq) * LEAF_M + tid] =
-                    (t <= n && m >= w) ? ld(&p.C[cell_index(n, sp, t) * pitch + (m - w)], fresh) : INFINITY;
-            }
-        }
-    }
-    for (int r = SB - 1; r >= 0; r--) {
-        if (r < SB - 1) leaf_wait(my_flags, q, (phase_id << 4) | (SB - 1 - r));
-        __syncthreads();  // rows below: other chunks (flags) and this chunk (CS_) complete
-        const int s = s0 + r;
-        if (live && s <= n) {
-            double AL[SB - 1], part[SB], AR[SB + 1];
-#pragma unroll
-            for (int k = 0; k < SB - 1; k++)
-                AL[k] = (s + k + 1 <= ea) ? ld(&p.A[a_index(s, s + k) * pitch + m], fresh) : INFINITY;
-#pragma unroll
-            for (int c = 0; c < SB; c++)
-                part[c] = (partial && t0 + c <= n) ? __ldcg(&p.C[cell_index(n, s, t0 + c) * pitch + m]) : INFINITY;
-            AR[0] = __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]);
-#pragma unroll
-            for (int c = 0; c < SB; c++) {
-                const int t = t0 + c;
-                if (t > n) break;
-                double c1 = INFINITY;
-                if (m >= m_null(p, s, t)) {  // every shifted index below is >= 0 (DESIGN Q6)
-                    double best = part[c];
-#pragma unroll
-                    for (int k = 0; k < SB - 1; k++) {  // left: rows below in this sub-tile
-                        const int sp = s + k + 1;
-                        if (sp > ea) break;
-                        const int mm = m - p.wx[sp - 1];
-                        const double cv = (mm >= m0) ? CS_[((sp - s0) * SB + c) * LEAF_M + (mm - m0)]
-                                                     : __ldcg(&p.C[cell_index(n, sp, t) * pitch + mm]);
-                        best = dmin(best, __dadd_rn(AL[k], cv));
-                    }
-#pragma unroll
-                    for (int cq = 0; cq <= c; cq++)  // right: staged column sub-block
-                        best = dmin(best, __dadd_rn(AR[cq], RS_[(c * (c + 1) / 2 + cq) * LEAF_M + tid]));
-                    c1 = best;
-                }
-                double cc = c1;
-                if (!p.restricted && m >= m_all(p, s, t)) {  // F_all: row s+1 at m - wbx[s] >= 0
-                    const int mm = m - p.wbx[s];
-                    const double sub_v = (s + 1 <= ea && mm >= m0)
-                                             ? CS_[((s + 1 - s0) * SB + c) * LEAF_M + (mm - m0)]
-                                             : __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + mm]);
-                    cc = dmin(cc, __dadd_rn(p.w[s], sub_v));
-                }
-                p.C[cell_index(n, s, t) * pitch + m] = cc;
-                CS_[(r * SB + c) * LEAF_M + tid] = cc;
-                const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), cc);
-                if (t < n) p.A[a_index(s, t) * pitch + m] = a;
-                AR[c + 1] = a;
-            }
-        }
-        __syncthreads();  // row r of this chunk complete (global and CS_)
-        leaf_publish(my_flags + q, (phase_id << 4) | (SB - r));
-    }
-}
-
-// Off-diagonal leaf, column-parallel: CTA = LEAF_CM consecutive m x the SB
-// columns of one sub-tile, lane = (m, column c), c = lane % SB; the rows go
-// bottom-up as in k_sub_leaf (same look-back flags, chunks of LEAF_CM m).
-// What a lane keeps in registers for the whole sub-tile:
-//   Cr[cq] = C(t0+cq, t, m - wx[t0+cq-1])  right operand of split s' = t0+cq <= t
-//            (final before this launch: column sub-block gamma of (J,J));
-//   Lc[k]  = C(s0+k+1, t, m - wx[s0+k])    left operand of split s' = s0+k+1,
-//            the same for every row above s', loaded once right after row s'
-//            is done (this launch: behind the row barrier / look-back flags).
-// The row's own A operands A(s, t0+cq-1) travel along the row with a shuffle
-// inside the SB-lane group: lane cq-1 finishes its cell, then every lane
-// c >= cq takes the split s' = t0+cq.  Per row a lane loads only the
-// partial, the F_all operand, the new left operand and A(s, ·) (shared by
-// the group), instead of every split's C operand.
-constexpr int LEAF_CM = 32;             // m per CTA
-constexpr int LEAF_CT = LEAF_CM * SB;   // 256 threads
-
-__global__ void __launch_bounds__(LEAF_CT, 3) k_sub_leaf_col(Problem p, int delta, int e, int *flags, int phase_id,
-                                                              int tile_lo) {
-    const int n = p.n, S = p.S;
-    const int64_t pitch = p.pitch;
-    const int n_chunks = (S + 1 + LEAF_CM - 1) / LEAF_CM;
-    const int cnt = sub_count(delta, e);
-    const int q = blockIdx.x % n_chunks;
-    const int sub = blockIdx.x / n_chunks;
-    int alpha, gamma;
-    sub_at(delta, e, sub % cnt, alpha, gamma);
-    const int I = tile_lo + sub / cnt, J = I + delta;
-    const int i0 = I * TB + 1, j0 = J * TB + 1;
-    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
-    if (s0 > n || t0 > n) return;  // sub-tiles past the last stage: no cells (uniform for the whole sub-tile)
-    const int c = threadIdx.x % SB;
-    const int m0 = q * LEAF_CM;
-    const int m = m0 + threadIdx.x / SB;
-    const int t = t0 + c;
-    const bool live = m <= S && t <= n;  // this lane owns column t at m
-    const bool fresh = (delta == 0);     // right C and left A of this tile diagonal (see k_sub_leaf)
-    const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
-    int *my_flags = flags + (int64_t)sub * n_chunks;
-    // per-sub-tile tables in shared memory (no global round trip on the row path)
-    __shared__ int s_mnull[SB][SB], s_mall[SB][SB], s_wx[SB], s_wbx[SB];
-    __shared__ double s_w[SB], s_Ps[SB], s_Pt[SB];
-    __shared__ int s_qlo;
-    if (threadIdx.x < SB * SB) {
-        const int rr = threadIdx.x / SB, cc = threadIdx.x % SB, ss = s0 + rr, tt = t0 + cc;
-        const bool ok = ss <= n && tt <= n;  // ss < tt for off-diagonal sub-tiles
-        s_mnull[rr][cc] = ok ? m_null(p, ss, tt) : INT_MAX;
-        s_mall[rr][cc] = ok && !p.restricted ? m_all(p, ss, tt) : INT_MAX;
-        if (cc == 0) {
-            const bool row = ss < n;  // rows s < t <= n
-            s_wx[rr] = row ? p.wx[ss] : 0;    // shift of split s' = ss + 1
-            s_wbx[rr] = row ? p.wbx[ss] : 0;  // F_all shift of row ss
-            s_w[rr] = row ? p.w[ss] : 0.0;
-            s_Ps[rr] = ss <= n ? p.P[ss - 1] : 0.0;
-            s_Pt[rr] = p.P[min(t0 + rr, n)];
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {  // lowest chunk any shifted read of this sub-tile can reach
-        int wmax = 0;
-        for (int k = 0; k < SB; k++) wmax = max(wmax, max(s_wx[k], s_wbx[k]));
-        s_qlo = m0 - wmax <= 0 ? 0 : (m0 - wmax) / LEAF_CM;
-    }
-
-    double Cr[SB];
-#pragma unroll
-    for (int cq = 0; cq < SB; cq++) {
-        const int sp = t0 + cq;
-        const int w = cq <= c && live ? p.wx[sp - 1] : 0;
-        Cr[cq] = (live && cq <= c && m >= w) ? ld(&p.C[cell_index(n, sp, t) * pitch + (m - w)], fresh) : INFINITY;
-    }
-    double Lc[SB - 1];
-#pragma unroll
-    for (int k = 0; k < SB - 1; k++) Lc[k] = INFINITY;
-    __syncthreads();
-    const int q_lo = s_qlo;
-
-#pragma unroll
-    for (int r = SB - 1; r >= 0; r--) {
-        const int s = s0 + r;
-        if (r < SB - 1) {
-            const int need = (phase_id << 4) | (SB - 1 - r);  // rows SB-1 .. r+1 done
-            for (int qq = q_lo + (int)threadIdx.x; qq < q; qq += LEAF_CT) {
-                int v;
-                do {
-                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(my_flags + qq) : "memory");
-                } while (v < need);
-            }
-            __syncthreads();
-        }
-        if (s <= n) {  // uniform over the CTA
-            // every load of the row in one round trip
-            const bool gate = live && m >= s_mnull[r][c];  // every shifted index >= 0 under it (DESIGN Q6)
-            const bool gall = live && m >= s_mall[r][c];   // F_all: row s+1 at m - wbx[s] >= 0
-            if (r < SB - 1) {  // row s+1 = s0+r+1 is complete at every m: its left operand for the rows above
-                const int w = s_wx[r];
-                Lc[r] = (live && m >= w) ? __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - w)]) : INFINITY;
-            }
-            const double fv = gall ? __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - s_wbx[r])]) : INFINITY;
-            double best = (gate && partial) ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
-            double al[SB - 1];
-#pragma unroll
-            for (int k = r; k < SB - 1; k++)  // left: s' = s0+k+1 in (s, ea], A(s, s'-1)
-                al[k] = gate ? ld(&p.A[a_index(s, s0 + k) * pitch + m], fresh) : INFINITY;
-            const double ar0 = live ? __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]) : INFINITY;  // A(s, t0-1)
-            if (gate) {
-#pragma unroll
-                for (int k = r; k < SB - 1; k++) best = dmin(best, __dadd_rn(al[k], Lc[k]));
-            }
-            const double F = gall ? __dadd_rn(s_w[r], fv) : INFINITY;
-            const double u = __dadd_rn(s_Pt[c], -s_Ps[r]);
-            double myA = INFINITY, cc = INFINITY;
-#pragma unroll
-            for (int cq = 0; cq < SB; cq++) {  // right: s' = t0+cq, operand A(s, t0+cq-1) from lane cq-1
-                const double a = cq == 0 ? ar0 : __shfl_sync(0xffffffffu, myA, cq - 1, SB);
-                if (gate && c >= cq) best = dmin(best, __dadd_rn(a, Cr[cq]));
-                if (c == cq) {
-                    cc = dmin(best, F);  // best = +inf when the m_null gate is closed
-                    myA = __dadd_rn(u, cc);
-                }
-            }
-            if (live) {
-                p.C[cell_index(n, s, t) * pitch + m] = cc;
-                if (t < n) p.A[a_index(s, t) * pitch + m] = myA;
-            }
-        }
-        __syncthreads();  // every lane of this chunk finished row r
-        if (threadIdx.x == 0)  // release (cumulative over the barrier): the chunk's row r is visible
-            asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(my_flags + q), "r"((phase_id << 4) | (SB - r))
-                         : "memory");
-    }
-}
+// (Rejected variants, measured and removed: a column-parallel leaf — thread =
+// (m, column), the row chain by warp shuffles, 327 vs 291 ms — and a leaf with
+// both the right-range operands and its own results in shared memory, 147 vs
+// 119 ms at the time; profiles/r01_tiled_v4.md, r01_tiled_v5.md.)
 
 // Flags of the leaf look-back: one int per (sub-tile of a phase, m-chunk).
 inline size_t leaf_flag_bytes(int L, int S) {
     const int nb = (L + 1 + TB - 1) / TB;
-    const int chunks = max((S + 1 + LEAF_M - 1) / LEAF_M, (S + 1 + LEAF_CM - 1) / LEAF_CM);
+    const int chunks = (S + 1 + LEAF_M - 1) / LEAF_M;
     return (size_t)nb * NSB * chunks * sizeof(int);
 }
 
-// Off-diagonal leaf kernel: k_sub_leaf<false> (row: thread = m), k_sub_leaf_col
-// (thread = (m, column)) or k_sub_leaf_smem; ROTOR_LEAF=row|col|smem selects
-// one for measurements (default: the fastest measured, LEAF_VARIANT_DEFAULT).
-enum { LEAF_VARIANT_ROW = 0, LEAF_VARIANT_COL = 1, LEAF_VARIANT_SMEM = 2, LEAF_VARIANT_TAB = 3, LEAF_VARIANT_TABR = 4 };
-constexpr int LEAF_VARIANT_DEFAULT = LEAF_VARIANT_TABR;  // 243.6 ms per config-4 solve (tab 265.7, row 268)
+// Off-diagonal leaf kernel: k_sub_leaf<false> (row: thread = m, scalars from
+// global), k_sub_leaf_row<false> (scalars staged in shared memory) or
+// k_sub_leaf_row<true> (also the right-range operands; the default, the fastest
+// measured); ROTOR_LEAF=row|tab|tabr selects one for A/B measurements.
+enum { LEAF_VARIANT_ROW = 0, LEAF_VARIANT_TAB = 1, LEAF_VARIANT_TABR = 2 };
+constexpr int LEAF_VARIANT_DEFAULT = LEAF_VARIANT_TABR;
 inline int leaf_variant() {
     static const int v = [] {
         const char *e = getenv("ROTOR_LEAF");
         if (!e) return (int)LEAF_VARIANT_DEFAULT;
-        if (!strcmp(e, "col")) return (int)LEAF_VARIANT_COL;
-        if (!strcmp(e, "smem")) return (int)LEAF_VARIANT_SMEM;
         if (!strcmp(e, "tab")) return (int)LEAF_VARIANT_TAB;
         if (!strcmp(e, "tabr")) return (int)LEAF_VARIANT_TABR;
         return (int)LEAF_VARIANT_ROW;
@@ -909,7 +665,6 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
     if (ntiles <= 0) return 0;
     const int n_mg = (p.S + 1 + 15) / 16;  // product: a warp per (sub-tile, 16 m)
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
-    const int n_chunks_col = (p.S + 1 + LEAF_CM - 1) / LEAF_CM;
     const int phases = delta == 0 ? NSB : 2 * NSB - 1;
     int launches = 0;
     for (int e = 0; e < phases; e++) {
@@ -936,14 +691,10 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
         const int lb = ntiles * cnt * n_chunks;
         if (delta == 0 && e == 0)
             k_sub_leaf<true><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
-        else if (leaf_variant() == LEAF_VARIANT_COL)
-            k_sub_leaf_col<<<ntiles * cnt * n_chunks_col, LEAF_CT, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else if (leaf_variant() == LEAF_VARIANT_TAB)
             k_sub_leaf_row<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else if (leaf_variant() == LEAF_VARIANT_TABR)
             k_sub_leaf_row<true><<<lb, LEAF_M, NPAIR * LEAF_M * 8, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
-        else if (leaf_variant() == LEAF_VARIANT_SMEM)
-            k_sub_leaf_smem<<<lb, LEAF_M, LEAF_SMEM, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else
             k_sub_leaf<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         launches++;

@@ -1,6 +1,6 @@
 #!/usr/bin/env bash
 # A/B timing of kernel variants selected by environment variables (run on the GPU box).
-# Usage: VAR=ROTOR_LEAF VALUES="row tab col" PYTEST_K=tiled bash scripts/gpu_variants.sh <tag>
+# Usage: VAR=ROTOR_LEAF VALUES="row tab tabr" PYTEST_K=tiled bash scripts/gpu_variants.sh <tag>
 set -u
 TAG=${1:-v}
 OUT=gpurun_out/$TAG
