@@ -156,6 +156,11 @@ constexpr int PW = DEP_THREADS / 32;
 __device__ __forceinline__ void cp_async8(double *dst, const double *src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
+// src_bytes = 0: nothing is read, the 8 bytes are zero-filled
+__device__ __forceinline__ void cp_async8_zfill(double *dst, const double *src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(valid ? 8 : 0)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -203,28 +208,43 @@ __global__ void __launch_bounds__(DEP_THREADS, 4) k_sub_product_async(Problem p,
     __syncwarp();
     const int64_t pitch = p.pitch;
     const bool mlive = m <= S;
-    // split idx: 0..n1-1 -> s' = lo1 + idx (left), n1.. -> s' = lo2 + idx - n1 (right)
-    auto issue = [&](int idx) {
-        double(*st)[SB][16] = ring[wid][idx % PNS];
-        const bool r2 = idx >= n1;
-        const int q = r2 ? lo2 + (idx - n1) : lo1 + idx;
-        const int w = r2 ? ws[TB + idx - n1] : ws[idx];
-        const bool use = mlive && m >= w;  // else +inf: every cell it feeds is gated (m < w <= m_null)
-        // rows s0+jh.. of A column q-1 and cells (q, t0+jh..) are consecutive rows of their tables
-        const double *ga = p.A + a_index(s0 + jh, q - 1) * pitch + m;
-        const double *gc = p.C + cell_index(n, q, t0 + jh) * pitch + (m - w);
+    // split idx: 0..n1-1 -> s' = lo1 + idx (left), n1.. -> s' = lo2 + idx - n1 (right).
+    // Issued in order, so the lane walks its operand rows incrementally: rows
+    // s0+jh.. of A column q-1 and cells (q, t0+jh..) are consecutive table rows,
+    // A column q-1 -> q moves a_index by q-1 rows, cell (q,t) -> (q+1,t) moves
+    // cell_index by n-q rows (s-major).
+    const int64_t pitch4[PH] = {0, pitch, 2 * pitch, 3 * pitch};
+    unsigned rows_a = 0, rows_c = 0;  // which of the lane's rows / columns exist
+#pragma unroll
+    for (int i = 0; i < PH; i++) {
+        rows_a |= (s0 + jh + i <= n) << i;
+        rows_c |= (t0 + jh + i <= n) << i;
+    }
+    int nx = 0, q = n1 > 0 ? lo1 : lo2;
+    const double *pa = p.A + a_index(s0 + jh, q - 1) * pitch + m;
+    const double *pc = p.C + cell_index(n, q, t0 + jh) * pitch + m;
+    auto issue_next = [&]() {
+        double(*st)[SB][16] = ring[wid][nx % PNS];
+        const int w = nx < n1 ? ws[nx] : ws[TB + nx - n1];
+        // A skipped operand is zero-filled: m < w means every cell the split
+        // feeds is gated (m < w <= m_null, DESIGN Q6), so its partial is never
+        // read; a row / column past the last stage feeds only cells that do not
+        // exist.  Branch-free copies (src-size 0 reads nothing).
+        const bool use = mlive && m >= w;
+        const double *pcw = use ? pc - w : pc;
 #pragma unroll
         for (int i = 0; i < PH; i++) {
-            const int row = jh + i;  // this lane copies A row `row` and C column `row`
-            double *da = &st[0][row][mi], *dc = &st[1][row][mi];
-            if (use && s0 + row <= n)
-                cp_async8(da, ga + i * pitch);
-            else
-                *da = INFINITY;
-            if (use && t0 + row <= n)
-                cp_async8(dc, gc + i * pitch);
-            else
-                *dc = INFINITY;
+            cp_async8_zfill(&st[0][jh + i][mi], pa + pitch4[i], use && ((rows_a >> i) & 1));
+            cp_async8_zfill(&st[1][jh + i][mi], pcw + pitch4[i], use && ((rows_c >> i) & 1));
+        }
+        if (++nx == n1 && n2 > 0) {  // on to the right range
+            q = lo2;
+            pa = p.A + a_index(s0 + jh, q - 1) * pitch + m;
+            pc = p.C + cell_index(n, q, t0 + jh) * pitch + m;
+        } else {
+            pa += (int64_t)(q - 1) * pitch;
+            pc += (int64_t)(n - q) * pitch;
+            q++;
         }
     };
     double acc[SB][PH];
@@ -238,11 +258,11 @@ __global__ void __launch_bounds__(DEP_THREADS, 4) k_sub_product_async(Problem p,
         }
 #pragma unroll
     for (int k = 0; k < PNS - 1; k++) {
-        if (k < nsp) issue(k);
+        if (k < nsp) issue_next();
         cp_async_commit();
     }
     for (int idx = 0; idx < nsp; idx++) {
-        if (idx + PNS - 1 < nsp) issue(idx + PNS - 1);
+        if (idx + PNS - 1 < nsp) issue_next();
         cp_async_commit();
         cp_async_wait<PNS - 1>();  // split idx landed (this lane's copies)
         __syncwarp();              // ... and every lane's
