@@ -167,8 +167,9 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
-__global__ void __launch_bounds__(DEP_THREADS, 4) k_sub_product_async(Problem p, int delta, int e, int tile_lo,
-                                                                      int ntiles) {
+template <int MINB>
+__global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product_async(Problem p, int delta, int e, int tile_lo,
+                                                                         int ntiles) {
     __shared__ int wxs[PW][2 * TB];
     __shared__ double ring[PW][PNS][2][SB][16];  // [warp][stage][A | C][row | column][m]
     const int n = p.n, S = p.S;
@@ -247,15 +248,20 @@ __global__ void __launch_bounds__(DEP_THREADS, 4) k_sub_product_async(Problem p,
             q++;
         }
     };
+    // the lane's cells (s0+i, t0+jh+j): row i starts cell_index(n, s0+i, t0+jh),
+    // rows s -> s+1 are n-s cells apart (s-major), columns consecutive
     double acc[SB][PH];
+    {
+        const double *cr = p.C + cell_index(n, s0, t0 + jh) * pitch + m;
 #pragma unroll
-    for (int i = 0; i < SB; i++)
+        for (int i = 0; i < SB; i++) {
 #pragma unroll
-        for (int j = 0; j < PH; j++) {
-            const int s = s0 + i, t = t0 + jh + j;
-            acc[i][j] = (partial && mlive && s <= n && t <= n) ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m])
-                                                              : INFINITY;
+            for (int j = 0; j < PH; j++)
+                acc[i][j] = (partial && mlive && s0 + i <= n && ((rows_c >> j) & 1)) ? __ldcg(cr + pitch4[j])
+                                                                                       : INFINITY;
+            cr += (int64_t)(n - (s0 + i)) * pitch;
         }
+    }
 #pragma unroll
     for (int k = 0; k < PNS - 1; k++) {
         if (k < nsp) issue_next();
@@ -279,13 +285,15 @@ __global__ void __launch_bounds__(DEP_THREADS, 4) k_sub_product_async(Problem p,
         __syncwarp();  // stage idx % PNS is refilled by the next iteration's issue
     }
     if (!mlive) return;
+    double *cw = p.C + cell_index(n, s0, t0 + jh) * pitch + m;
 #pragma unroll
-    for (int i = 0; i < SB; i++)
+    for (int i = 0; i < SB; i++) {
+        if (s0 + i > n) break;
 #pragma unroll
-        for (int j = 0; j < PH; j++) {
-            const int s = s0 + i, t = t0 + jh + j;
-            if (s <= n && t <= n) p.C[cell_index(n, s, t) * pitch + m] = acc[i][j];
-        }
+        for (int j = 0; j < PH; j++)
+            if ((rows_c >> j) & 1) cw[pitch4[j]] = acc[i][j];
+        cw += (int64_t)(n - (s0 + i)) * pitch;
+    }
 }
 
 // Finish cell (s,t) at m from its running minimum c1 (already gated): F_all
@@ -662,10 +670,10 @@ inline int leaf_variant() {
     return v;
 }
 
-// Product kernel: ROTOR_PROD=1 k_sub_product_async (default: 266.7 vs 268.3
-// ms per config-4 solve), 3 / 4 k_sub_product at 3 CTAs/SM (<= 170
-// registers, no spill) / 4 (<= 128, small spill) — same time.
-constexpr int PRODUCT_MINB_DEFAULT = 1;
+// Product kernel: ROTOR_PROD=2 k_sub_product_async at 3 CTAs/SM (default:
+// 222.4 ms per config-4 solve), 1 the same at 4 CTAs/SM (223.2), 3 / 4
+// k_sub_product (operands through registers) at 3 / 4 CTAs/SM (231.4).
+constexpr int PRODUCT_MINB_DEFAULT = 2;
 inline int product_minb() {
     static const int v = [] {
         const char *e = getenv("ROTOR_PROD");
@@ -701,7 +709,9 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
         }
         if (has_product) {
             if (product_minb() == 1)
-                k_sub_product_async<<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
+                k_sub_product_async<4><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
+            else if (product_minb() == 2)
+                k_sub_product_async<3><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
             else if (product_minb() == 4)
                 k_sub_product<4><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
             else
