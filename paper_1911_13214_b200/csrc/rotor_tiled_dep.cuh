@@ -467,6 +467,9 @@ struct LeafTab {
     int wxr[SB];                      // wxr[c] = wx[t0+c-1]: shift of the right split s' = t0+c
     int wbx[SB];                      // wbx[s0+r]: F_all shift of row r
     double w[SB], Ps[SB], Pt[SB];     // w[s0+r], P[s0+r-1], P[t0+c]
+    int64_t crow[SB + 1];             // element offset of C cell (s0+j, t0) (columns t0+c follow, pitch apart)
+    int64_t arow[SB];                 // element offset of A(s0+r, t0-1)
+    int64_t aleft[SB][SB - 1];        // element offset of A(s0+r, s0+r+k) (left split s' = s0+r+k+1)
     int q_lo;                         // lowest m-chunk a shifted read of a row below can reach
 };
 
@@ -485,7 +488,11 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
             T.w[rr] = row ? p.w[ss] : 0.0;
             T.Ps[rr] = ss <= n ? p.P[ss - 1] : 0.0;
             T.Pt[rr] = p.P[min(t0 + rr, n)];
+            T.arow[rr] = ss <= n ? a_index(ss, t0 - 1) * p.pitch : 0;
         }
+        if (cc < SB - 1) T.aleft[rr][cc] = ss + cc < n ? a_index(ss, ss + cc) * p.pitch : 0;
+        if (threadIdx.x <= SB) T.crow[threadIdx.x] = s0 + (int)threadIdx.x <= n
+                                                          ? cell_index(n, s0 + threadIdx.x, t0) * p.pitch : 0;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -507,18 +514,22 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     // operands written by earlier launches first — their loads are in flight
     // during the look-back wait: A(s, ·) of the left splits, A(s, t0-1), and
     // the partial minimum of the row's cells
+    // addresses from the staged row offsets: cells (s, t0+c) are consecutive rows
+    const double *Cm = p.C + m;
+    double *Cw = p.C + m;
     double AL[SB - 1];  // AL[k] = A(s, s + k): left split s' = s + k + 1 <= ea
 #pragma unroll
     for (int k = 0; k < SB - 1; k++)
-        AL[k] = (live && k < SB - 1 - r) ? ld(&p.A[a_index(s, s + k) * pitch + m], fresh) : INFINITY;
+        AL[k] = (live && k < SB - 1 - r) ? ld(p.A + T.aleft[r][k] + m, fresh) : INFINITY;
     double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
-    AR[0] = live ? __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]) : INFINITY;
+    AR[0] = live ? __ldcg(p.A + T.arow[r] + m) : INFINITY;
     double B[SB], F[SB];
     bool gate[SB];
+    const int64_t crow = T.crow[r];
 #pragma unroll
     for (int c = 0; c < SB; c++) {
         gate[c] = live && m >= T.mnull[r][c];  // INT_MAX past the last stage
-        B[c] = (gate[c] && partial) ? __ldcg(&p.C[cell_index(n, s, t0 + c) * pitch + m]) : INFINITY;
+        B[c] = (gate[c] && partial) ? __ldcg(Cm + crow + c * pitch) : INFINITY;
     }
     wait();  // the rows below are complete at every m this row reads (flags + barrier)
     if (!live) return;
@@ -531,14 +542,12 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
             for (int k = 0; k < SB - 1; k++) {  // left: C of the rows below in this sub-tile
                 if (k >= SB - 1 - r) break;
                 const int j = r + k + 1;  // s' = s0 + j
-                const double cv = __ldcg(&p.C[cell_index(n, s0 + j, t) * pitch + (m - T.wxl[j])]);
+                const double cv = __ldcg(Cm + T.crow[j] + c * pitch - T.wxl[j]);
                 best = dmin(best, __dadd_rn(AL[k], cv));
             }
         }
         B[c] = best;
-        F[c] = m >= T.mall[r][c]
-                   ? __dadd_rn(T.w[r], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - T.wbx[r])]))
-                   : INFINITY;
+        F[c] = m >= T.mall[r][c] ? __dadd_rn(T.w[r], __ldcg(Cm + T.crow[r + 1] + c * pitch - T.wbx[r])) : INFINITY;
     }
     if (RS) cp_async_wait<0>();  // this thread's right-range operands are in shared memory
 #pragma unroll
@@ -558,7 +567,7 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
             c1 = best;
         }
         const double cc = dmin(c1, F[c]);
-        p.C[cell_index(n, s, t) * pitch + m] = cc;
+        Cw[crow + c * pitch] = cc;
         const double a = __dadd_rn(__dadd_rn(T.Pt[c], -T.Ps[r]), cc);
         if (t < n) p.A[a_index(s, t) * pitch + m] = a;
         AR[c + 1] = a;
