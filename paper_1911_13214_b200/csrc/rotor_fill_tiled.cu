@@ -41,7 +41,11 @@ constexpr int STAGES = 3;   // TMA pipeline depth (2 stages in flight while one 
 // stages amortise the per-stage barrier wait / arrive / refill.
 constexpr int CONSUMERS = 512;  // 16 warps: two per scheduler slot more than 8 hide the DADD->DSETP->FSEL chain
 constexpr int THREADS = CONSUMERS;
-constexpr int RS = 4, RT = 8;            // register tile (s x t) per consumer thread (<= 128 registers)
+// Register tile (s x t) per consumer thread (<= 128 registers).  8 x 4 rather
+// than 4 x 8: the two half-warps (adjacent t groups) share the 8 A values, so
+// an A load is one shared-memory wavefront and only the 4 C loads are two
+// (16 wavefronts per split instead of 20): 217.2 vs 222.0 ms per solve.
+constexpr int RS = 8, RT = 4;
 static_assert((TB / RS) * (TB / RT) * TM == CONSUMERS, "one thread per (m, register tile)");
 // A TMA box must start on a 16-byte boundary of the row (an odd fp64 start
 // column faults with "illegal instruction", scripts/tma_probe.cu): the shifted
@@ -209,7 +213,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
     const int mi = tid & 15;
     const int g = tid >> 4;
-    const int sg = g >> 2, tg = g & 3;
+    const int sg = g / (TB / RT), tg = g % (TB / RT);  // register-tile row / column group
     for (int kl = 0; kl < my_items; kl++) {
     double acc[RS][RT];
 #pragma unroll
