@@ -206,7 +206,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     // The producer is lane 0 of the LAST warp: the warp scheduler favours the
     // highest warp id, so the refills are not delayed behind the consumers
     // (with warp 0 as producer ~19% of the warp time was spent waiting for
-    // TMA data, profiles/r01_tiled_v4.md).
+    // TMA data, profiles/r01_tiled_v4.md).  A dedicated 17th producer warp does
+    // not fit: the register file is split per scheduler (16 K registers each),
+    // and 5 warps on one scheduler cap every thread at 96 registers.
     constexpr int PRODUCER = CONSUMERS - 32;
     if (tid == PRODUCER)
         for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);

@@ -535,7 +535,6 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     if (!live) return;
 #pragma unroll
     for (int c = 0; c < SB; c++) {
-        const int t = t0 + c;
         double best = B[c];
         if (gate[c]) {
 #pragma unroll
