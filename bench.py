@@ -257,33 +257,64 @@ def run_batched(args):
     width = max(len(l) for l in my_limits)
     counted = sum(R.transitions(ch.L, S) * len(l) for ch, l in zip(my_chains, my_limits))
     my_limits = [l + [l[-1]] * (width - len(l)) for l in my_limits]
+    # algorithmic HBM bytes of the fused kernel: one wavefront per table (DESIGN §5.1 model)
+    counted_bytes = sum(alg_bytes_wavefront(ch.L, S) * len(l) for ch, l in zip(my_chains, my_limits))
     stream = torch.cuda.current_stream()
     for _ in range(args.warmup):
         R.solve_batch(my_chains, my_limits, S, with_ops=True, stream=stream)
     torch.cuda.synchronize()
     if pg:
         pg.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         R.solve_batch(my_chains, my_limits, S, with_ops=True, stream=stream)
     e1.record(stream)
     torch.cuda.synchronize()
+    clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    c = torch.tensor([counted], dtype=torch.float64, device=dev)
+    c = torch.tensor([counted, counted_bytes], dtype=torch.float64, device=dev)
     if pg:
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
         pg.all_reduce(c, op=pg.ReduceOp.SUM)
     if rank == 0:
-        tot = float(c.item())
+        tot, tot_bytes = float(c[0].item()), float(c[1].item())
+        sec = float(t.item()) / 1e3
+        peaks, peak_kind = measured_peaks()
+        achieved = tot_bytes * args.steps / sec / 1e9
+        peak = float(peaks["hbm_gbs"]) * world
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            import oracle as O
+
+            O.build()
+            stride = 4  # bounded sample: every 4th limit of every chain (the whole limit range)
+            js = list(range(stride - 1, nl, stride))
+            t0 = time.perf_counter()
+            for i, ch in enumerate(chains):
+                for j in js:
+                    O.OracleSolve(ch, limits[i][j], S)
+            dtc = time.perf_counter() - t0
+            trc = sum(R.transitions(ch.L, S) * len(js) for ch in chains)
+            cpu = {"value": trc / dtc, "unit": UNIT, "cores": 1, "kind": "oracle",
+                   "sample": f"oracle solves of every {stride}th limit of each of the 8 chains "
+                             f"({len(chains) * len(js)} tables, {trc:.3e} transitions, {dtc:.1f} s, single thread)"}
         line = {"metric": "DP cell-transitions/sec, batched 256-limit x 8-chain sweep (config 5)",
-                "value": tot * args.steps / (float(t.item()) / 1e3), "unit": UNIT, "n_gpus": world,
+                "value": tot * args.steps / sec, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": {"workload": "cfg5_sweep_8x256_S500", "problems": len(chains) * nl,
                                                  "transitions_per_step": tot, "S": S,
-                                                 "note": "host-buffer API: H2D chains/limits and D2H costs+ops inside the timed region"}}
+                                                 "note": "host-buffer API: H2D chains/limits and D2H costs+ops inside the timed region"},
+                "clocks": clk,
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                             "kernel": "k_batch (fused: discretise, limits, wavefront fill, Algorithm 2 per table)",
+                             "alg_bytes_per_step": tot_bytes},
+                "cpu_baseline": cpu, "gpu_launches": args.steps * world}
         print(json.dumps(line), flush=True)
     if pg:
         pg.destroy_process_group()
