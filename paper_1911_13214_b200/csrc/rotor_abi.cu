@@ -434,6 +434,12 @@ int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_ch
             total_ops += h_cap[q];
         }
     }
+    // queue order: the longest chains first (cost ~ L^3 at a common S): the
+    // short tables fill the tail instead of a long one starting last
+    std::vector<int32_t> h_order(P);
+    for (int64_t q = 0; q < P; q++) h_order[q] = (int32_t)q;
+    std::stable_sort(h_order.begin(), h_order.end(),
+                     [&](int32_t x, int32_t y) { return Ls[h_pc[x]] > Ls[h_pc[y]]; });
     const int n_slots = (int)std::min<int64_t>(P, 2 * (int64_t)sms);
     const size_t slot = rotor::batch_slot_bytes(L_max, slots);
     // one device allocation (library cache): descriptors, outputs, ops, then the slot pool
@@ -446,7 +452,7 @@ int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_ch
     const size_t o_d = take(h_d.size() * 8), o_u = take(h_u.size() * 8), o_pc = take(P * 4), o_L = take(n_chains * 4),
                  o_lim = take(P * 8), o_off = take(P * 8), o_cap = take(P * 8), o_cost = take(P * 8),
                  o_nops = take(P * 8), o_st = take(P * 4), o_ops = take((size_t)std::max<int64_t>(total_ops, 1) * 8),
-                 o_ctr = take(8), o_pool = take((size_t)n_slots * slot);
+                 o_ctr = take(8), o_ord = take(P * 4), o_pool = take((size_t)n_slots * slot);
     void *wsv = nullptr;
     int r = cached_workspace(off, &wsv);
     if (r) return r;
@@ -458,6 +464,7 @@ int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_ch
     CK(cudaMemcpyAsync(w + o_lim, limits, P * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(w + o_off, h_off.data(), P * 8, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(w + o_cap, h_cap.data(), P * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_ord, h_order.data(), P * 4, cudaMemcpyHostToDevice, st));
     CK(cudaMemsetAsync(w + o_ctr, 0, 8, st));
     rotor::BatchArgs b{};
     b.n_problems = (int)P;
@@ -483,6 +490,7 @@ int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_ch
     b.ops_off = (const int64_t *)(w + o_off);
     b.ops_cap = (const int64_t *)(w + o_cap);
     b.counter = (int *)(w + o_ctr);
+    b.order = (const int32_t *)(w + o_ord);
     rotor::launch_batch(b, n_slots, st);
     CK(cudaGetLastError());
     std::vector<int64_t> h_n(P);

@@ -1,7 +1,8 @@
 // Fused batched solver: many independent (chain, limit)
 // tables — the paper's multi-limit sweep, "Algorithm 1 for 10 different memory
 // limits" — in ONE launch.  A persistent CTA takes problems from an
-// atomic queue and runs the whole path for each inside its own workspace slot:
+// atomic queue (handed out longest chain first, so the tail is short) and runs
+// the whole path for each inside its own workspace slot:
 // precompute (discretisation with that limit's slot size M/S),
 // leaf, every diagonal d (barrier between diagonals), Algorithm-2 walk.  The
 // per-cell arithmetic is the wavefront kernel's (rotor_device.cuh), so every
@@ -50,7 +51,10 @@ __global__ void __launch_bounds__(512) k_batch(BatchArgs b) {
     const SlotLayout y = slot_layout(b.L_max, b.S);
     char *slot = b.pool + (size_t)blockIdx.x * y.bytes;
     while (true) {
-        if (threadIdx.x == 0) prob = atomicAdd(b.counter, 1);
+        if (threadIdx.x == 0) {
+            const int k = atomicAdd(b.counter, 1);
+            prob = k < b.n_problems ? b.order[k] : b.n_problems;
+        }
         __syncthreads();
         const int pi = prob;
         __syncthreads();
