@@ -46,7 +46,7 @@ struct Layout {
     int stack_cap = 0;
     int64_t ops_cap = 0;
     size_t off_wx, off_wbx, off_wy, off_of, off_ob, off_P, off_w, off_mnull, off_stack, off_res;
-    size_t off_chain, off_ops, off_C, off_D, off_A, off_tiled;
+    size_t off_chain, off_ops, off_C, off_D, off_A, off_C32, off_A32, off_tiled;
     size_t total = 0;
     bool has_D = false;
     bool has_A = false;
@@ -98,6 +98,8 @@ Layout make_layout(int L, int S, const rotor_options &o) {
     y.off_D = y.has_D ? take((size_t)y.cells * y.pitch * 2) : 0;
     y.has_A = uses_tiled(o);
     y.off_A = y.has_A ? take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 8) : 0;
+    y.off_C32 = y.has_A ? take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 4) : 0;
+    y.off_A32 = y.has_A ? take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 4) : 0;
     y.off_tiled = take(rotor::tiled_extra_bytes(L, S));
     y.total = off;
     return y;
@@ -123,6 +125,8 @@ rotor::Problem make_problem(const Layout &y, char *ws, const rotor_options &o) {
     p.C = (double *)(ws + y.off_C) + rotor::kPad;  // column m = 0 of row 0
     p.D = y.has_D ? (uint16_t *)(ws + y.off_D) + rotor::kPad : nullptr;
     p.A = y.has_A ? (double *)(ws + y.off_A) + rotor::kPad : nullptr;
+    p.C32 = y.has_A ? (float *)(ws + y.off_C32) + rotor::kPad : nullptr;
+    p.A32 = y.has_A ? (float *)(ws + y.off_A32) + rotor::kPad : nullptr;
     p.flags = y.has_A ? (int *)(ws + y.off_tiled) : nullptr;
     p.res_cost = (double *)(ws + y.off_res);
     p.res_nops = (int64_t *)(ws + y.off_res + 8);

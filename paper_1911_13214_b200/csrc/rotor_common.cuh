@@ -37,6 +37,9 @@ struct Problem {
     uint16_t *D;  // nullable
     double *A;    // nullable: A(s,c,m) = fl(fl(P[c]-P[s-1]) + C(s,c,m)), row a_index(s,c) (tiled fill)
     int *flags;   // nullable: tiled fill's leaf look-back flags (tiled_extra_bytes)
+    // nullable (tiled fill): fp32 round-down shadows of C and A, same rows and
+    // pitch (in elements), read by the pruned middle kernel's lower-bound filter
+    float *C32, *A32;
     // reconstruction / results
     int4 *stack;
     int32_t stack_cap;
@@ -66,6 +69,17 @@ __device__ __forceinline__ int m_all(const Problem &p, int s, int t) {
 
 __device__ __forceinline__ int m_null(const Problem &p, int s, int t) {
     return p.mnullT[(int64_t)(t - 1) * p.n + (s - 1)];
+}
+
+// Store a finished cell's C and A with their fp32 round-down shadows
+// (cvt.rm: a lower bound of the fp64 value, +inf stays +inf).
+__device__ __forceinline__ void store_final_c(const Problem &p, int64_t off, double c) {
+    p.C[off] = c;
+    if (p.C32) p.C32[off] = __double2float_rd(c);
+}
+__device__ __forceinline__ void store_final_a(const Problem &p, int64_t off, double a) {
+    p.A[off] = a;
+    if (p.A32) p.A32[off] = __double2float_rd(a);
 }
 
 }  // namespace rotor

@@ -69,9 +69,13 @@ __device__ __forceinline__ void leaf_cell(const Problem &p, int s, int m) {
     const int ma = m_all(p, s, s);
     const int64_t off = cell_index(p.n, s, s) * p.pitch + m;
     const double c = (m >= ma) ? p.w[s] : INFINITY;
-    p.C[off] = c;
     if (p.D) p.D[off] = (m >= ma) ? 0 : kNone;
-    if (p.A && s < p.n) p.A[a_index(s, s) * p.pitch + m] = __dadd_rn(__dadd_rn(p.P[s], -p.P[s - 1]), c);
+    if (p.A) {
+        store_final_c(p, off, c);
+        if (s < p.n) store_final_a(p, a_index(s, s) * p.pitch + m, __dadd_rn(__dadd_rn(p.P[s], -p.P[s - 1]), c));
+    } else {
+        p.C[off] = c;
+    }
 }
 
 // Eq. (2) for one cell (s, t = s+d, m), candidates in Algorithm 2's order:

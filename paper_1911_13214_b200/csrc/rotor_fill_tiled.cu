@@ -270,6 +270,765 @@ __global__ void __launch_bounds__(THREADS, 1)
     }  // items
 }
 
+// ---------------------------------------------------------------------------
+// Pruned middle (default): the same partial minimum with most of the fp64
+// candidates skipped by an exact fp32 lower-bound filter.
+//
+// For a candidate v = fl64(a + b) with a, b >= 0 (or +inf), the fp32 value
+//     lb = fadd_rd( cvt_rd(a), cvt_rd(b) )
+// satisfies lb <= a + b, and since lb is also an fp64 number and rounding is
+// monotone, lb <= fl64(a + b) = v.  So if the minimum of lb over a chunk of KC
+// splits is >= the running fp64 minimum acc of a cell, no candidate of the
+// chunk can lower acc, and skipping them leaves acc bit-identical (the min is
+// exact; ties do not matter because the fill keeps values, not argmins).
+// cvt.rm maps +inf to +inf and finite values above FLT_MAX to FLT_MAX, so the
+// bound holds for every input.  Cost per candidate: FADD.RM + FMNMX on the
+// fp32/ALU pipes instead of DADD + DSETP (half rate) + 2 SEL; a warp runs the
+// exact fp64 chunk only when one of its 16 m x 32 cells can improve (about
+// one chunk in eight at config 4 in ascending s' order: the running minimum
+// settles early, DESIGN 5.2).
+// The fp32 copies of a stage are made once per CTA (each warp converts 1/16
+// of the stage) and published through a per-stage mbarrier.
+// ---------------------------------------------------------------------------
+template <int KC_, int STAGES_>
+struct PrunedRing {
+    static constexpr int KC = KC_, STAGES = STAGES_;
+    static constexpr int A_ST = KC * TB * TM, B_ST = KC * TB * TMB;  // doubles per stage
+    static constexpr size_t bytes = (size_t)STAGES * (A_ST + B_ST) * 12  // fp64 boxes + fp32 copies
+                                    + 3 * STAGES * 8 + STAGES * KC * 4 + 64;
+};
+
+template <int KC_, int STAGES_>
+__global__ void __launch_bounds__(THREADS, 1)
+    k_tile_middle_pruned(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
+                         Problem p, int delta, int tile_lo, int n_tiles) {
+    using R = PrunedRing<KC_, STAGES_>;
+    constexpr int KC = R::KC, STAGES = R::STAGES, A_ST = R::A_ST, B_ST = R::B_ST;
+    extern __shared__ __align__(1024) double smem[];
+    double *As = smem;                                         // [STAGES][KC][TB][TM]
+    double *Bs = As + STAGES * A_ST;                           // [STAGES][KC][TB][TMB]
+    float *Af = reinterpret_cast<float *>(Bs + STAGES * B_ST);  // fp32 round-down copies, same layout
+    float *Bf = Af + STAGES * A_ST;
+    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + STAGES * B_ST);
+    uint64_t *empty = full + STAGES;
+    uint64_t *conv = empty + STAGES;                     // fp32 copy of stage complete (16 warp arrivals)
+    int *soff = reinterpret_cast<int *>(conv + STAGES);  // [STAGES][KC]
+    int *wx_s = soff + STAGES * KC;
+
+    const int n = p.n;
+    const int n_mc = (p.S + 1 + TM - 1) / TM;
+    const int n_items = n_tiles * n_mc;
+    if ((int)blockIdx.x >= n_items) return;
+    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int iters = (delta - 1) * TB / KC;
+    const int total = my_items * iters;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int *wxp = p.wx;
+    if (n <= WX_SMEM_MAX) {
+        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
+        wxp = wx_s;
+    }
+
+    auto issue = [&](int gi) {  // as k_tile_middle
+        const int st = gi % STAGES;
+        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        const int i0 = I * TB + 1, j0 = J * TB + 1, m0 = (item % n_mc) * TM;
+        const int sp0 = i0 + TB + (gi % iters) * KC;
+        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 1;
+        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 8));
+        for (int k = 0; k < KC; k++)
+            tma_load_2d(As + st * A_ST + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
+        for (int k = 0; k < KC; k++) {
+            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
+            tma_load_2d(Bs + st * B_ST + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp0 + k, j0), &full[st]);
+        }
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CONSUMERS / 32);
+            mbar_init(&conv[s], CONSUMERS / 32);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int PRODUCER = CONSUMERS - 32;
+    if (tid == PRODUCER)
+        for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);
+
+    const int mi = tid & 15;
+    const int g = tid >> 4;
+    const int sg = g / (TB / RT), tg = g % (TB / RT);
+    constexpr int PAIRS = (A_ST + B_ST) / 2;  // double2 per stage
+    for (int kl = 0; kl < my_items; kl++) {
+        double acc[RS][RT];
+#pragma unroll
+        for (int i = 0; i < RS; i++)
+#pragma unroll
+            for (int j = 0; j < RT; j++) acc[i][j] = INFINITY;
+
+        for (int it = 0; it < iters; it++) {
+            const int gi = kl * iters + it;
+            const int st = gi % STAGES;
+            const uint32_t par = (uint32_t)((gi / STAGES) & 1);
+            mbar_wait(&full[st], par);
+            {  // this warp's share of the stage's fp32 copy
+                const double2 *a2 = reinterpret_cast<const double2 *>(As + st * A_ST);
+                const double2 *b2 = reinterpret_cast<const double2 *>(Bs + st * B_ST);
+                float2 *af2 = reinterpret_cast<float2 *>(Af + st * A_ST);
+                float2 *bf2 = reinterpret_cast<float2 *>(Bf + st * B_ST);
+                for (int q = tid; q < PAIRS; q += THREADS) {
+                    const bool isA = q < A_ST / 2;
+                    const double2 v = isA ? a2[q] : b2[q - A_ST / 2];
+                    const float2 f = make_float2(__double2float_rd(v.x), __double2float_rd(v.y));
+                    if (isA) af2[q] = f; else bf2[q - A_ST / 2] = f;
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&conv[st]);
+            }
+            mbar_wait(&conv[st], par);
+            // filter: per cell the minimum lower bound over the KC splits
+            float mn[RS][RT];
+            {
+                const float *a_f = Af + st * A_ST + (sg * RS) * TM + mi;
+                const float *b_f = Bf + st * B_ST + (tg * RT) * TMB + mi;
+#pragma unroll
+                for (int k = 0; k < KC; k++) {
+                    float a[RS], b[RT];
+                    const float *bk = b_f + k * TB * TMB + soff[st * KC + k];
+#pragma unroll
+                    for (int i = 0; i < RS; i++) a[i] = a_f[k * TB * TM + i * TM];
+#pragma unroll
+                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
+#pragma unroll
+                    for (int i = 0; i < RS; i++)
+#pragma unroll
+                        for (int j = 0; j < RT; j++) {
+                            const float v = __fadd_rd(a[i], b[j]);
+                            mn[i][j] = k == 0 ? v : fminf(mn[i][j], v);
+                        }
+                }
+            }
+            bool need = false;
+#pragma unroll
+            for (int i = 0; i < RS; i++)
+#pragma unroll
+                for (int j = 0; j < RT; j++) need |= (double)mn[i][j] < acc[i][j];
+            if (__any_sync(0xffffffffu, need)) {  // exact fp64 chunk (as k_tile_middle)
+                const double *a_s = As + st * A_ST + (sg * RS) * TM + mi;
+                const double *b_s = Bs + st * B_ST + (tg * RT) * TMB + mi;
+#pragma unroll
+                for (int k = 0; k < KC; k++) {
+                    double a[RS], b[RT];
+                    const double *bk = b_s + k * TB * TMB + soff[st * KC + k];
+#pragma unroll
+                    for (int i = 0; i < RS; i++) a[i] = a_s[k * TB * TM + i * TM];
+#pragma unroll
+                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
+#pragma unroll
+                    for (int i = 0; i < RS; i++)
+#pragma unroll
+                        for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (tid == PRODUCER && gi + STAGES < total) {
+                mbar_wait(&empty[st], par);
+                issue(gi + STAGES);
+            }
+        }
+
+        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        const int i0 = I * TB + 1, j0 = J * TB + 1;
+        const int m = (item % n_mc) * TM + mi;
+        if (m <= p.S) {
+#pragma unroll
+            for (int i = 0; i < RS; i++) {
+                const int s = i0 + sg * RS + i;
+#pragma unroll
+                for (int j = 0; j < RT; j++) {
+                    const int t = j0 + tg * RT + j;
+                    if (t <= n) p.C[cell_index(n, s, t) * p.pitch + m] = acc[i][j];
+                }
+            }
+        }
+    }
+}
+// Decoupled variant: the fp64 boxes land in a 2-slot TMA ring that is
+// released as soon as every warp has converted its share into a separate
+// 2-slot fp32 ring; a warp converts chunk gi+1 before filtering chunk gi, so a
+// warp that lags by up to one chunk (an exact pass) does not stall the others,
+// and both fp64 slots are in flight while a chunk is filtered.  The rare exact
+// chunk reads its fp64 operands from global memory (L2: the TMA just fetched
+// them).  Same values as the TMA boxes on every non-gated cell (a C operand
+// at m - wx < 0 is +inf there; below -kPad the boxes are clamped, but those
+// cells are gated, DESIGN Q6).
+struct Pruned2Ring {
+    static constexpr int KC = 8, S64 = 2, S32 = 2;
+    static constexpr int A_ST = KC * TB * TM, B_ST = KC * TB * TMB;
+    static constexpr size_t bytes = (size_t)S64 * (A_ST + B_ST) * 8 + (size_t)S32 * (A_ST + B_ST) * 4 +
+                                    (2 * S64 + 2 * S32) * 8 + S32 * KC * 4 + 64;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_tile_middle_pruned2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
+                          Problem p, int delta, int tile_lo, int n_tiles) {
+    using R = Pruned2Ring;
+    constexpr int KC = R::KC, S64 = R::S64, S32 = R::S32, A_ST = R::A_ST, B_ST = R::B_ST;
+    extern __shared__ __align__(1024) double smem[];
+    double *As = smem;                                         // [S64][KC][TB][TM]
+    double *Bs = As + S64 * A_ST;                              // [S64][KC][TB][TMB]
+    float *Af = reinterpret_cast<float *>(Bs + S64 * B_ST);    // [S32][KC][TB][TM]
+    float *Bf = Af + S32 * A_ST;                               // [S32][KC][TB][TMB]
+    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + S32 * B_ST);  // fp64 slot landed (TMA tx)
+    uint64_t *empty = full + S64;                              // fp64 slot converted by all 16 warps
+    uint64_t *conv = empty + S64;                              // fp32 slot ready (16 warps)
+    uint64_t *free32 = conv + S32;                             // fp32 slot consumed (16 warps)
+    int *soff = reinterpret_cast<int *>(free32 + S32);         // [S32][KC] box column offsets
+    int *wx_s = soff + S32 * KC;
+
+    const int n = p.n;
+    const int n_mc = (p.S + 1 + TM - 1) / TM;
+    const int n_items = n_tiles * n_mc;
+    if ((int)blockIdx.x >= n_items) return;
+    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int iters = (delta - 1) * TB / KC;
+    const int total = my_items * iters;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int *wxp = p.wx;
+    if (n <= WX_SMEM_MAX) {
+        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
+        wxp = wx_s;
+    }
+    auto coords = [&](int gi, int &i0, int &j0, int &m0, int &sp0) {
+        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        i0 = I * TB + 1;
+        j0 = J * TB + 1;
+        m0 = (item % n_mc) * TM;
+        sp0 = i0 + TB + (gi % iters) * KC;
+    };
+    auto issue = [&](int gi) {
+        const int st = gi % S64;
+        int i0, j0, m0, sp0;
+        coords(gi, i0, j0, m0, sp0);
+        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 8));
+        for (int k = 0; k < KC; k++)
+            tma_load_2d(As + st * A_ST + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
+        for (int k = 0; k < KC; k++) {
+            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
+            tma_load_2d(Bs + st * B_ST + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp0 + k, j0), &full[st]);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < S64; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CONSUMERS / 32);
+        }
+        for (int s = 0; s < S32; s++) {
+            mbar_init(&conv[s], CONSUMERS / 32);
+            mbar_init(&free32[s], CONSUMERS / 32);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int PRODUCER = CONSUMERS - 32;
+    if (tid == PRODUCER)
+        for (int gi = 0; gi < S64 && gi < total; gi++) issue(gi);
+
+    const int warp = tid >> 5;
+    // chunk gi: fp64 slot gi % S64 -> fp32 slot gi % S32 (this warp's 1/16 share)
+    auto convert = [&](int gi) {
+        const int s64 = gi % S64, s32 = gi % S32;
+        if (gi >= S32) mbar_wait(&free32[s32], (uint32_t)(((gi - S32) / S32) & 1));  // chunk gi-S32 consumed
+        mbar_wait(&full[s64], (uint32_t)((gi / S64) & 1));
+        if (lane == 0) {  // box column offsets of this chunk (read by the filter after conv)
+            if (warp == 0) {
+                int i0, j0, m0, sp0;
+                coords(gi, i0, j0, m0, sp0);
+                for (int k = 0; k < KC; k++) soff[s32 * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 1;
+            }
+        }
+        constexpr int PA = A_ST / 2, PT = (A_ST + B_ST) / 2, PER = PT / (CONSUMERS / 32);
+        const double2 *a2 = reinterpret_cast<const double2 *>(As + s64 * A_ST);
+        const double2 *b2 = reinterpret_cast<const double2 *>(Bs + s64 * B_ST);
+        float2 *af2 = reinterpret_cast<float2 *>(Af + s32 * A_ST);
+        float2 *bf2 = reinterpret_cast<float2 *>(Bf + s32 * B_ST);
+        static_assert(PT % (CONSUMERS / 32) == 0, "even conversion shares");
+#pragma unroll 3
+        for (int q = warp * PER + lane; q < (warp + 1) * PER; q += 32) {
+            const double2 v = q < PA ? a2[q] : b2[q - PA];
+            const float2 f = make_float2(__double2float_rd(v.x), __double2float_rd(v.y));
+            if (q < PA) af2[q] = f; else bf2[q - PA] = f;
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&empty[s64]);
+            mbar_arrive(&conv[s32]);
+        }
+    };
+
+    const int mi = tid & 15;
+    const int g = tid >> 4;
+    const int sg = g / (TB / RT), tg = g % (TB / RT);
+    // once every warp has converted chunk c, its fp64 slot takes chunk c + S64
+    auto refill = [&](int c) {
+        if (tid == PRODUCER && c + S64 < total) {
+            mbar_wait(&empty[c % S64], (uint32_t)((c / S64) & 1));
+            issue(c + S64);
+        }
+    };
+    if (total > 0) {
+        convert(0);
+        refill(0);
+    }
+    for (int kl = 0; kl < my_items; kl++) {
+        double acc[RS][RT];
+#pragma unroll
+        for (int i = 0; i < RS; i++)
+#pragma unroll
+            for (int j = 0; j < RT; j++) acc[i][j] = INFINITY;
+        for (int it = 0; it < iters; it++) {
+            const int gi = kl * iters + it;
+            if (gi + 1 < total) {
+                convert(gi + 1);
+                refill(gi + 1);
+            }
+            const int s32 = gi % S32;
+            mbar_wait(&conv[s32], (uint32_t)((gi / S32) & 1));
+            float mn[RS][RT];
+            {
+                const float *a_f = Af + s32 * A_ST + (sg * RS) * TM + mi;
+                const float *b_f = Bf + s32 * B_ST + (tg * RT) * TMB + mi;
+#pragma unroll
+                for (int k = 0; k < KC; k++) {
+                    float a[RS], b[RT];
+                    const float *bk = b_f + k * TB * TMB + soff[s32 * KC + k];
+#pragma unroll
+                    for (int i = 0; i < RS; i++) a[i] = a_f[k * TB * TM + i * TM];
+#pragma unroll
+                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
+#pragma unroll
+                    for (int i = 0; i < RS; i++)
+#pragma unroll
+                        for (int j = 0; j < RT; j++) {
+                            const float v = __fadd_rd(a[i], b[j]);
+                            mn[i][j] = k == 0 ? v : fminf(mn[i][j], v);
+                        }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&free32[s32]);
+            bool need = false;
+#pragma unroll
+            for (int i = 0; i < RS; i++)
+#pragma unroll
+                for (int j = 0; j < RT; j++) need |= (double)mn[i][j] < acc[i][j];
+            if (__any_sync(0xffffffffu, need)) {  // exact fp64 chunk, operands from global memory
+                int i0, j0, m0, sp0;
+                coords(gi, i0, j0, m0, sp0);
+                const int m = min(m0 + mi, p.S);
+                const int s_0 = i0 + sg * RS, t_0 = j0 + tg * RT;
+#pragma unroll 2
+                for (int k = 0; k < KC; k++) {
+                    const int sp = sp0 + k;
+                    const int mm = m - wxp[sp - 1];
+                    double a[RS], b[RT];
+                    const double *ap = p.A + a_index(s_0, sp - 1) * p.pitch + m;
+#pragma unroll
+                    for (int i = 0; i < RS; i++) a[i] = __ldcg(ap + (int64_t)i * p.pitch);
+                    const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
+#pragma unroll
+                    for (int j = 0; j < RT; j++)
+                        b[j] = (mm >= 0 && t_0 + j <= n) ? __ldcg(bp + (int64_t)j * p.pitch) : INFINITY;
+#pragma unroll
+                    for (int i = 0; i < RS; i++)
+#pragma unroll
+                        for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
+                }
+            }
+        }
+        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        const int i0 = I * TB + 1, j0 = J * TB + 1;
+        const int m = (item % n_mc) * TM + mi;
+        if (m <= p.S) {
+#pragma unroll
+            for (int i = 0; i < RS; i++) {
+                const int s = i0 + sg * RS + i;
+#pragma unroll
+                for (int j = 0; j < RT; j++) {
+                    const int t = j0 + tg * RT + j;
+                    if (t <= n) p.C[cell_index(n, s, t) * p.pitch + m] = acc[i][j];
+                }
+            }
+        }
+    }
+}
+
+// Variant 3: fp64 boxes in a 5-slot TMA ring of KC = 4 splits (three slots in
+// flight while one is filtered), their fp32 copies in a separate 2-slot ring;
+// a warp converts its share of chunk gi+1 before filtering chunk gi (one chunk
+// of slack between warps); per cell an fp32 upper bound of the running
+// minimum (bestf = cvt_ru(acc)) so the filter is FADD.RM + FSETP.OR per
+// candidate with no per-chunk check; the exact pass reads the fp64 slot.
+struct Pruned3Ring {
+    static constexpr int KC = 4, S64 = 5, S32 = 2;
+    static constexpr int A_ST = KC * TB * TM, B_ST = KC * TB * TMB;
+    static constexpr size_t bytes = (size_t)S64 * (A_ST + B_ST) * 8 + (size_t)S32 * (A_ST + B_ST) * 4 +
+                                    (2 * S64 + 2 * S32) * 8 + (S64 + S32) * KC * 4 + 64;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_tile_middle_pruned3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
+                          Problem p, int delta, int tile_lo, int n_tiles) {
+    using R = Pruned3Ring;
+    constexpr int KC = R::KC, S64 = R::S64, S32 = R::S32, A_ST = R::A_ST, B_ST = R::B_ST;
+    extern __shared__ __align__(1024) double smem[];
+    double *As = smem;                                         // [S64][KC][TB][TM]
+    double *Bs = As + S64 * A_ST;                              // [S64][KC][TB][TMB]
+    float *Af = reinterpret_cast<float *>(Bs + S64 * B_ST);    // [S32][KC][TB][TM]
+    float *Bf = Af + S32 * A_ST;                               // [S32][KC][TB][TMB]
+    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + S32 * B_ST);  // fp64 slot landed (TMA tx)
+    uint64_t *empty = full + S64;                              // fp64 slot done (16 warps)
+    uint64_t *conv = empty + S64;                              // fp32 slot ready (16 warps)
+    uint64_t *free32 = conv + S32;                             // fp32 slot consumed (16 warps)
+    int *soff = reinterpret_cast<int *>(free32 + S32);         // [S64][KC] box column offsets
+    int *wx_s = soff + (S64 + S32) * KC;
+
+    const int n = p.n;
+    const int n_mc = (p.S + 1 + TM - 1) / TM;
+    const int n_items = n_tiles * n_mc;
+    if ((int)blockIdx.x >= n_items) return;
+    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int iters = (delta - 1) * TB / KC;
+    const int total = my_items * iters;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int *wxp = p.wx;
+    if (n <= WX_SMEM_MAX) {
+        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
+        wxp = wx_s;
+    }
+    auto issue = [&](int gi) {
+        const int st = gi % S64;
+        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        const int i0 = I * TB + 1, j0 = J * TB + 1, m0 = (item % n_mc) * TM;
+        const int sp0 = i0 + TB + (gi % iters) * KC;
+        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 1;
+        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 8));
+        for (int k = 0; k < KC; k++)
+            tma_load_2d(As + st * A_ST + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
+        for (int k = 0; k < KC; k++) {
+            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
+            tma_load_2d(Bs + st * B_ST + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp0 + k, j0), &full[st]);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < S64; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CONSUMERS / 32);
+        }
+        for (int s = 0; s < S32; s++) {
+            mbar_init(&conv[s], CONSUMERS / 32);
+            mbar_init(&free32[s], CONSUMERS / 32);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int PRODUCER = CONSUMERS - 32;
+    if (tid == PRODUCER)
+        for (int gi = 0; gi < S64 && gi < total; gi++) issue(gi);
+
+    const int warp = tid >> 5;
+    auto convert = [&](int gi) {  // this warp's 1/16 share of chunk gi: fp64 slot -> fp32 slot
+        const int s64 = gi % S64, s32 = gi % S32;
+        if (gi >= S32) mbar_wait(&free32[s32], (uint32_t)(((gi - S32) / S32) & 1));
+        mbar_wait(&full[s64], (uint32_t)((gi / S64) & 1));
+        constexpr int PA = A_ST / 2, PT = (A_ST + B_ST) / 2, PER = PT / (CONSUMERS / 32);
+        static_assert(PT % (CONSUMERS / 32) == 0, "even conversion shares");
+        const double2 *a2 = reinterpret_cast<const double2 *>(As + s64 * A_ST);
+        const double2 *b2 = reinterpret_cast<const double2 *>(Bs + s64 * B_ST);
+        float2 *af2 = reinterpret_cast<float2 *>(Af + s32 * A_ST);
+        float2 *bf2 = reinterpret_cast<float2 *>(Bf + s32 * B_ST);
+#pragma unroll
+        for (int q = warp * PER + lane; q < (warp + 1) * PER; q += 32) {
+            const double2 v = q < PA ? a2[q] : b2[q - PA];
+            const float2 f = make_float2(__double2float_rd(v.x), __double2float_rd(v.y));
+            if (q < PA) af2[q] = f; else bf2[q - PA] = f;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[s32]);
+    };
+
+    const int mi = tid & 15;
+    const int g = tid >> 4;
+    const int sg = g / (TB / RT), tg = g % (TB / RT);
+    if (total > 0) convert(0);
+    for (int kl = 0; kl < my_items; kl++) {
+        double acc[RS][RT];
+        float bestf[RS][RT];  // fp32 upper bound of acc
+#pragma unroll
+        for (int i = 0; i < RS; i++)
+#pragma unroll
+            for (int j = 0; j < RT; j++) {
+                acc[i][j] = INFINITY;
+                bestf[i][j] = INFINITY;
+            }
+        for (int it = 0; it < iters; it++) {
+            const int gi = kl * iters + it;
+            if (gi + 1 < total) convert(gi + 1);
+            const int s32 = gi % S32, s64 = gi % S64;
+            mbar_wait(&conv[s32], (uint32_t)((gi / S32) & 1));
+            bool need = false;
+            {
+                const float *a_f = Af + s32 * A_ST + (sg * RS) * TM + mi;
+                const float *b_f = Bf + s32 * B_ST + (tg * RT) * TMB + mi;
+#pragma unroll
+                for (int k = 0; k < KC; k++) {
+                    float a[RS], b[RT];
+                    const float *bk = b_f + k * TB * TMB + soff[s64 * KC + k];
+#pragma unroll
+                    for (int i = 0; i < RS; i++) a[i] = a_f[k * TB * TM + i * TM];
+#pragma unroll
+                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
+#pragma unroll
+                    for (int i = 0; i < RS; i++)
+#pragma unroll
+                        for (int j = 0; j < RT; j++) need |= __fadd_rd(a[i], b[j]) < bestf[i][j];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&free32[s32]);
+            if (__any_sync(0xffffffffu, need)) {  // exact fp64 chunk from the fp64 slot
+                const double *a_s = As + s64 * A_ST + (sg * RS) * TM + mi;
+                const double *b_s = Bs + s64 * B_ST + (tg * RT) * TMB + mi;
+#pragma unroll
+                for (int k = 0; k < KC; k++) {
+                    double a[RS], b[RT];
+                    const double *bk = b_s + k * TB * TMB + soff[s64 * KC + k];
+#pragma unroll
+                    for (int i = 0; i < RS; i++) a[i] = a_s[k * TB * TM + i * TM];
+#pragma unroll
+                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
+#pragma unroll
+                    for (int i = 0; i < RS; i++)
+#pragma unroll
+                        for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
+                }
+#pragma unroll
+                for (int i = 0; i < RS; i++)
+#pragma unroll
+                    for (int j = 0; j < RT; j++) bestf[i][j] = __double2float_ru(acc[i][j]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s64]);
+            if (tid == PRODUCER && gi + S64 < total) {
+                mbar_wait(&empty[s64], (uint32_t)((gi / S64) & 1));
+                issue(gi + S64);
+            }
+        }
+        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        const int i0 = I * TB + 1, j0 = J * TB + 1;
+        const int m = (item % n_mc) * TM + mi;
+        if (m <= p.S) {
+#pragma unroll
+            for (int i = 0; i < RS; i++) {
+                const int s = i0 + sg * RS + i;
+#pragma unroll
+                for (int j = 0; j < RT; j++) {
+                    const int t = j0 + tg * RT + j;
+                    if (t <= n) p.C[cell_index(n, s, t) * p.pitch + m] = acc[i][j];
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Pruned middle on the fp32 shadow tables (default).  The leaf kernels store,
+// with every final C and A value, its round-down fp32 copy (store_final_*), so
+// the TMA ring carries only fp32 boxes (half the bytes of the fp64 boxes: six
+// 36 KB stages, five in flight) and there is nothing to convert on chip.
+// Per cell the thread keeps acc (exact fp64 running minimum) and bestf =
+// cvt_ru(acc) >= acc; a candidate fl64(a + b) can lower acc only if
+// fadd_rd(a32, b32) < bestf (a32 = cvt_rd(a) <= a, b32 <= b, so the fp32 sum
+// rounded down is <= a + b, and by monotone rounding <= fl64(a + b)).  The
+// filter is FADD.RM + FSETP.OR per candidate; a warp whose chunk has any
+// passing candidate recomputes it exactly from the fp64 tables in global
+// memory (on every non-gated cell the same values as the boxes: m - wx >= 0
+// there; gated cells' partials are never used, DESIGN Q6).  The result is
+// bit-identical to k_tile_middle.
+// ---------------------------------------------------------------------------
+constexpr int TMB32 = TM + 4;  // fp32 C box: 16-byte aligned start column, offset 0..3
+struct F32Ring {
+    static constexpr int KC = 8, STAGES = 6;
+    static constexpr int A_ST = KC * TB * TM, B_ST = KC * TB * TMB32;  // floats per stage
+    static constexpr size_t bytes = (size_t)STAGES * (A_ST + B_ST) * 4 + 2 * STAGES * 8 + STAGES * KC * 4 + 64;
+};
+constexpr int F32_WX_MAX = (int)((227 * 1024 - F32Ring::bytes) / 4);
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_tile_middle_f32(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmC32,
+                      Problem p, int delta, int tile_lo, int n_tiles) {
+    using R = F32Ring;
+    constexpr int KC = R::KC, STAGES = R::STAGES, A_ST = R::A_ST, B_ST = R::B_ST;
+    extern __shared__ __align__(1024) float fsm[];
+    float *Af = fsm;                     // [STAGES][KC][TB s][TM]
+    float *Bf = Af + STAGES * A_ST;      // [STAGES][KC][TB t][TMB32]
+    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + STAGES * B_ST);
+    uint64_t *empty = full + STAGES;
+    int *soff = reinterpret_cast<int *>(empty + STAGES);  // [STAGES][KC]
+    int *wx_s = soff + STAGES * KC;
+
+    const int n = p.n;
+    const int n_mc = (p.S + 1 + TM - 1) / TM;
+    const int n_items = n_tiles * n_mc;
+    if ((int)blockIdx.x >= n_items) return;
+    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int iters = (delta - 1) * TB / KC;
+    const int total = my_items * iters;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31;
+    const int *wxp = p.wx;
+    if (n <= F32_WX_MAX) {
+        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
+        wxp = wx_s;
+    }
+    auto coords = [&](int gi, int &i0, int &j0, int &m0, int &sp0) {
+        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        i0 = I * TB + 1;
+        j0 = J * TB + 1;
+        m0 = (item % n_mc) * TM;
+        sp0 = i0 + TB + (gi % iters) * KC;
+    };
+    auto issue = [&](int gi) {
+        const int st = gi % STAGES;
+        int i0, j0, m0, sp0;
+        coords(gi, i0, j0, m0, sp0);
+        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 3;
+        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 4));
+        for (int k = 0; k < KC; k++)
+            tma_load_2d(Af + st * A_ST + k * TB * TM, &tmA32, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
+        for (int k = 0; k < KC; k++) {
+            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
+            tma_load_2d(Bf + st * B_ST + k * TB * TMB32, &tmC32, c0 & ~3, (int)cell_index(n, sp0 + k, j0),
+                        &full[st]);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CONSUMERS / 32);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int PRODUCER = CONSUMERS - 32;
+    if (tid == PRODUCER)
+        for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);
+
+    const int mi = tid & 15;
+    const int g = tid >> 4;
+    const int sg = g / (TB / RT), tg = g % (TB / RT);
+    for (int kl = 0; kl < my_items; kl++) {
+        double acc[RS][RT];
+        float bestf[RS][RT];  // cvt_ru(acc) >= acc
+#pragma unroll
+        for (int i = 0; i < RS; i++)
+#pragma unroll
+            for (int j = 0; j < RT; j++) {
+                acc[i][j] = INFINITY;
+                bestf[i][j] = INFINITY;
+            }
+        for (int it = 0; it < iters; it++) {
+            const int gi = kl * iters + it;
+            const int st = gi % STAGES;
+            mbar_wait(&full[st], (uint32_t)((gi / STAGES) & 1));
+            bool need = false;
+            {
+                const float *a_f = Af + st * A_ST + (sg * RS) * TM + mi;
+                const float *b_f = Bf + st * B_ST + (tg * RT) * TMB32 + mi;
+#pragma unroll
+                for (int k = 0; k < KC; k++) {
+                    float a[RS], b[RT];
+                    const float *bk = b_f + k * TB * TMB32 + soff[st * KC + k];
+#pragma unroll
+                    for (int i = 0; i < RS; i++) a[i] = a_f[k * TB * TM + i * TM];
+#pragma unroll
+                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB32];
+#pragma unroll
+                    for (int i = 0; i < RS; i++)
+#pragma unroll
+                        for (int j = 0; j < RT; j++) need |= __fadd_rd(a[i], b[j]) < bestf[i][j];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (tid == PRODUCER && gi + STAGES < total) {
+                mbar_wait(&empty[st], (uint32_t)((gi / STAGES) & 1));
+                issue(gi + STAGES);
+            }
+            if (__any_sync(0xffffffffu, need)) {  // exact fp64 chunk, operands from global memory
+                int i0, j0, m0, sp0;
+                coords(gi, i0, j0, m0, sp0);
+                const int m = min(m0 + mi, p.S);
+                const int s_0 = i0 + sg * RS, t_0 = j0 + tg * RT;
+#pragma unroll 2
+                for (int k = 0; k < KC; k++) {
+                    const int sp = sp0 + k;
+                    const int mm = m - wxp[sp - 1];
+                    double a[RS], b[RT];
+                    const double *ap = p.A + a_index(s_0, sp - 1) * p.pitch + m;
+#pragma unroll
+                    for (int i = 0; i < RS; i++) a[i] = __ldcg(ap + (int64_t)i * p.pitch);
+                    const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
+#pragma unroll
+                    for (int j = 0; j < RT; j++)
+                        b[j] = (mm >= 0 && t_0 + j <= n) ? __ldcg(bp + (int64_t)j * p.pitch) : INFINITY;
+#pragma unroll
+                    for (int i = 0; i < RS; i++)
+#pragma unroll
+                        for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
+                }
+#pragma unroll
+                for (int i = 0; i < RS; i++)
+#pragma unroll
+                    for (int j = 0; j < RT; j++) bestf[i][j] = __double2float_ru(acc[i][j]);
+            }
+        }
+        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        const int i0 = I * TB + 1, j0 = J * TB + 1;
+        const int m = (item % n_mc) * TM + mi;
+        if (m <= p.S) {
+#pragma unroll
+            for (int i = 0; i < RS; i++) {
+                const int s = i0 + sg * RS + i;
+#pragma unroll
+                for (int j = 0; j < RT; j++) {
+                    const int t = j0 + tg * RT + j;
+                    if (t <= n) p.C[cell_index(n, s, t) * p.pitch + m] = acc[i][j];
+                }
+            }
+        }
+    }
+}
+
+// (the wx copy sized by WX_SMEM_MAX leaves 1 KB of the 227 KB spare)
+static_assert(PrunedRing<8, 2>::bytes <= SMEM_BYTES + 512 && PrunedRing<4, 4>::bytes <= SMEM_BYTES + 512 &&
+                  Pruned2Ring::bytes <= SMEM_BYTES + 512 && Pruned3Ring::bytes <= SMEM_BYTES + 512,
+              "pruned rings fit the exact ring's allocation");
+
 #include "rotor_tiled_dep.cuh"
 
 // ---------------------------------------------------------------------------
@@ -300,6 +1059,19 @@ bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t pitch,
     return r == CUDA_SUCCESS;
 }
 
+bool make_map32(CUtensorMap *map, const float *base, int64_t rows, int64_t pitch, int box_cols, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)pitch, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)(pitch * 4)};
+    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 }  // namespace tiled
 
 // Scratch of the tiled fill beyond the A table (which is part of the Layout): the leaf flags.
@@ -315,14 +1087,27 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(k_tile_middle<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess)
+                                 (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tile_middle_pruned<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(SMEM_BYTES + 512 + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tile_middle_pruned<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(SMEM_BYTES + 512 + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tile_middle_pruned2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(SMEM_BYTES + 512 + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tile_middle_pruned3, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(SMEM_BYTES + 512 + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
+            cudaFuncSetAttribute(k_tile_middle_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+                cudaSuccess)
             return -1;
         attr = true;
     }
     const int n = p.n;
     const int64_t rows = (int64_t)n * (n + 1) / 2;
     if (!make_map(reinterpret_cast<CUtensorMap *>(ctx->tmA), p.A - kPad, rows + kPadRows, p.pitch, TM, TB) ||
-        !make_map(reinterpret_cast<CUtensorMap *>(ctx->tmC), p.C - kPad, rows + kPadRows, p.pitch, TMB, TB))
+        !make_map(reinterpret_cast<CUtensorMap *>(ctx->tmC), p.C - kPad, rows + kPadRows, p.pitch, TMB, TB) ||
+        !p.A32 || !p.C32 ||
+        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmA32), p.A32 - kPad, rows + kPadRows, p.pitch, TM, TB) ||
+        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmC32), p.C32 - kPad, rows + kPadRows, p.pitch, TMB32, TB))
         return -1;
     if (!p.flags || cudaMemsetAsync(p.flags, 0, leaf_flag_bytes(p.L, p.S), st) != cudaSuccess) return -1;
     ctx->phase_id = 0;
@@ -347,7 +1132,27 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
         const size_t smem = SMEM_BYTES + (p.n <= WX_SMEM_MAX ? (size_t)p.n * 4 : 0);
         const CUtensorMap &tmA = *reinterpret_cast<const CUtensorMap *>(ctx->tmA);
         const CUtensorMap &tmC = *reinterpret_cast<const CUtensorMap *>(ctx->tmC);
-        k_tile_middle<KC, STAGES><<<grid, THREADS, smem, st>>>(tmA, tmC, p, delta, tile_lo, tile_hi - tile_lo);
+        static int variant = -1;  // ROTOR_MIDDLE=exact|p82|p44|p2 (A/B runs)
+        if (variant < 0) {
+            const char *e = getenv("ROTOR_MIDDLE");
+            variant = (e && !strcmp(e, "exact")) ? 0 : (e && !strcmp(e, "p82")) ? 1 : (e && !strcmp(e, "p44")) ? 2 : (e && !strcmp(e, "p2")) ? 3 : (e && !strcmp(e, "p3")) ? 4 : 5;
+        }
+        const int nt = tile_hi - tile_lo;
+        const size_t psmem = smem + 512;
+        if (variant == 1)
+            k_tile_middle_pruned<8, 2><<<grid, THREADS, psmem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
+        else if (variant == 2)
+            k_tile_middle_pruned<4, 4><<<grid, THREADS, psmem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
+        else if (variant == 3)
+            k_tile_middle_pruned2<<<grid, THREADS, psmem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
+        else if (variant == 4)
+            k_tile_middle_pruned3<<<grid, THREADS, psmem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
+        else if (variant == 5)
+            k_tile_middle_f32<<<grid, THREADS, F32Ring::bytes + (p.n <= F32_WX_MAX ? (size_t)p.n * 4 : 0), st>>>(
+                *reinterpret_cast<const CUtensorMap *>(ctx->tmA32), *reinterpret_cast<const CUtensorMap *>(ctx->tmC32),
+                p, delta, tile_lo, nt);
+        else
+            k_tile_middle<KC, STAGES><<<grid, THREADS, smem, st>>>(tmA, tmC, p, delta, tile_lo, tile_hi - tile_lo);
         launches++;
     }
     return launches + launch_dependent(p, delta, tile_lo, tile_hi, st, p.flags, ctx->phase_id);
@@ -390,7 +1195,12 @@ __global__ void k_tile_pack(Problem p, int delta, int tile_lo, double *buf, int 
         if (unpack) {
             const double v = packed[m];
             crow[m] = v;
-            if (has_a) arow[m] = __dadd_rn(u, v);
+            if (p.C32) p.C32[(crow - p.C) + m] = __double2float_rd(v);
+            if (has_a) {
+                const double av = __dadd_rn(u, v);
+                arow[m] = av;
+                if (p.A32) p.A32[(arow - p.A) + m] = __double2float_rd(av);
+            }
         } else {
             packed[m] = crow[m];
         }

@@ -38,6 +38,8 @@ size_t tiled_extra_bytes(int L, int S);
 struct TiledCtx {
     alignas(64) unsigned char tmA[128];  // CUtensorMap of the A table
     alignas(64) unsigned char tmC[128];  // CUtensorMap of the C table
+    alignas(64) unsigned char tmA32[128];  // fp32 shadow of A
+    alignas(64) unsigned char tmC32[128];  // fp32 shadow of C
     int phase_id;                        // leaf launches so far (look-back flag epochs)
 };
 int tiled_nb(int n);  // number of TB-stage blocks

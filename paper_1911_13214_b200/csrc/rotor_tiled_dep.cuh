@@ -306,9 +306,9 @@ __device__ __forceinline__ double finish(const Problem &p, int s, int t, int m, 
         const double v = __dadd_rn(p.w[s], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - p.wbx[s])]));
         c = dmin(c, v);
     }
-    p.C[cell_index(n, s, t) * pitch + m] = c;
+    store_final_c(p, cell_index(n, s, t) * pitch + m, c);
     const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), c);
-    if (t < n) p.A[a_index(s, t) * pitch + m] = a;
+    if (t < n) store_final_a(p, a_index(s, t) * pitch + m, a);
     return a;
 }
 
@@ -407,9 +407,9 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
             c1 = best;
         }
         const double cc = dmin(c1, F[c]);
-        p.C[cell_index(n, s, t) * pitch + m] = cc;
+        store_final_c(p, cell_index(n, s, t) * pitch + m, cc);
         const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), cc);
-        if (t < n) p.A[a_index(s, t) * pitch + m] = a;
+        if (t < n) store_final_a(p, a_index(s, t) * pitch + m, a);
         AR[c + 1] = a;
     }
 }
@@ -516,7 +516,6 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     // the partial minimum of the row's cells
     // addresses from the staged row offsets: cells (s, t0+c) are consecutive rows
     const double *Cm = p.C + m;
-    double *Cw = p.C + m;
     double AL[SB - 1];  // AL[k] = A(s, s + k): left split s' = s + k + 1 <= ea
 #pragma unroll
     for (int k = 0; k < SB - 1; k++)
@@ -566,9 +565,9 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
             c1 = best;
         }
         const double cc = dmin(c1, F[c]);
-        Cw[crow + c * pitch] = cc;
+        store_final_c(p, crow + c * pitch + m, cc);
         const double a = __dadd_rn(__dadd_rn(T.Pt[c], -T.Ps[r]), cc);
-        if (t < n) p.A[a_index(s, t) * pitch + m] = a;
+        if (t < n) store_final_a(p, a_index(s, t) * pitch + m, a);
         AR[c + 1] = a;
     }
 }

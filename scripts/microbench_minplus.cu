@@ -4,6 +4,9 @@
 //   0: v < acc ? v : acc on doubles       (DADD + DSETP + 2 FSEL)
 //   1: 64-bit integer min on the bit patterns of non-negative doubles
 //   2: DADD only (upper bound of the fp64 pipe)
+//   4: fp32 lower-bound filter (cvt.rm.f32.f64 of the operands, FADD.RM, FMNMX;
+//      per 8 splits one exact compare of the chunk minimum against the fp64
+//      accumulator) — the pruned middle kernel's steady state with no exact pass
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mb microbench_minplus.cu
 #include <cstdio>
 #include <cstdint>
@@ -22,6 +25,32 @@ __global__ void __launch_bounds__(256) kern(double *out, int iters) {
     for (int i = 0; i < RS; i++)
 #pragma unroll
         for (int j = 0; j < RT; j++) acc[i][j] = 1e300;
+    if (MODE == 4) {
+        for (int it = 0; it < iters; it++) {
+            float mn[RS][RT];
+#pragma unroll
+            for (int k = 0; k < 8; k++) {
+                float a[RS], b[RT];
+#pragma unroll
+                for (int i = 0; i < RS; i++) a[i] = __double2float_rd(As[(k + it) & 7][i][lane]);
+#pragma unroll
+                for (int j = 0; j < RT; j++) b[j] = __double2float_rd(Bs[(k + it) & 7][j][lane]);
+#pragma unroll
+                for (int i = 0; i < RS; i++)
+#pragma unroll
+                    for (int j = 0; j < RT; j++) {
+                        const float v = __fadd_rd(a[i], b[j]);
+                        mn[i][j] = k == 0 ? v : fminf(mn[i][j], v);
+                    }
+            }
+            bool need = false;
+#pragma unroll
+            for (int i = 0; i < RS; i++)
+#pragma unroll
+                for (int j = 0; j < RT; j++) need |= (double)mn[i][j] < acc[i][j];
+            if (__any_sync(0xffffffffu, need)) acc[it & 7 & (RS - 1)][0] = (double)mn[0][0];
+        }
+    } else
     for (int it = 0; it < iters; it++) {
 #pragma unroll 4
         for (int k = 0; k < 8; k++) {
@@ -89,5 +118,7 @@ int main() {
     run<1, 8, 8>("int64-min");
     run<2, 4, 8>("dadd-only");
     run<2, 8, 8>("dadd-only");
+    run<4, 8, 4>("fp32 filter");
+    run<4, 4, 8>("fp32 filter");
     return 0;
 }
