@@ -147,6 +147,32 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def middle_transitions(L: int, S: int, TB: int = 32) -> int:
+    """Candidates the tiled fill's middle kernel evaluates per solve (DESIGN 5.2):
+    tiles (I, J) with J - I >= 2, real cells s in block I, t in block J, splits
+    s' in blocks I+1..J-1 (all (J-I-1)*TB of them), each at every m = 0..S."""
+    n = L + 1
+    nb = (n + TB - 1) // TB
+    tot = 0
+    for I in range(nb):
+        cs = min(n, TB * (I + 1)) - TB * I
+        for J in range(I + 2, nb):
+            ct = min(n, TB * (J + 1)) - TB * J
+            tot += cs * ct * (J - I - 1) * TB
+    return tot * (S + 1)
+
+
+def ncu_kernel_step_traffic(key: str, kernel: str):
+    """DRAM bytes of one kernel's launches in one solve (committed ncu launch-list summary)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            ent = json.load(f)[key]["per_kernel"]
+        return next((v["dram_bytes"] for k, v in ent.items() if kernel in k), None)
+    except Exception:
+        return None
+
+
 def ncu_step_traffic(key: str):
     """DRAM read+write bytes of all launches of one solve, from the committed ncu launch list summary."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -455,6 +481,8 @@ def run_ours(args):
 
     clocks = ClockSampler(local)
     fill_ms = []
+    mid_ms = []
+    mid_launches = 0
     total_launches = 0
     fill_launches = 0
     if pg:
@@ -468,6 +496,8 @@ def run_ours(args):
         R.solve_device(d_chain, L, M, S, ws, out, stream=stream, **opts)
         t = R.last_timings()  # syncs on this step's last event (phase events on the launch stream)
         fill_ms.append(t["fill_ms"])
+        mid_ms.append(t["middle_ms"])
+        mid_launches = t["middle_launches"]
         total_launches += t["total_launches"]
         fill_launches = t["fill_launches"]
     e1.record(stream)
@@ -520,23 +550,37 @@ def run_ours(args):
     peaks, peak_kind = measured_peaks()
     fill_avg_ms = sum(fill_ms) / len(fill_ms)
     if kernel in ("auto", "tiled"):
-        # Tiled fill: bound by the fp64 pipe: every transition is one
-        # DADD (64 lanes/clk/SM on B200) + one DSETP (half rate, 32 lanes/clk/SM), both
-        # on the fp64 pipe -> 1/64 + 1/32 clk per transition per lane-slot = 21.33
-        # transitions/clk/SM (the 2 FSEL go to the ALU pipe).
+        # Dominant kernel: the pruned middle (DESIGN 5.2).  Every candidate costs one
+        # FADD.RM (FMA pipe) + one FSETP.LT.OR on the ALU pipe (16 lanes/clk per SM
+        # sub-partition, 64 per SM); the rare exact fp64 recomputes run on the fp64
+        # pipe.  Peak = 148 SMs x 64 candidates/clk x sm_max_mhz.
         clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
-        peak = 148 * (64.0 / 3.0) * clk_mhz * 1e6 / 1e9  # Gtransitions/s
-        achieved = tr / (fill_avg_ms / 1e3) / 1e9
+        mid_avg_ms = sum(mid_ms) / len(mid_ms)
+        tm = middle_transitions(L, S)
+        peak = 148 * 64.0 * clk_mhz * 1e6 / 1e9  # Gtransitions/s
+        achieved = tm / (mid_avg_ms / 1e3) / 1e9
+        # the whole fill against the exact fp64 evaluation model (DADD 64 lanes/clk +
+        # DSETP 32 lanes/clk per SM on the fp64 pipe -> 21.33 transitions/clk/SM)
+        fill_peak = 148 * (64.0 / 3.0) * clk_mhz * 1e6 / 1e9
+        fill_ach = tr / (fill_avg_ms / 1e3) / 1e9
         roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gtransitions/s",
-                    "frac": achieved / peak, "traffic": ncu_step_traffic("tiled_solve"),
-                    "traffic_scope": "DRAM read+write bytes of every launch of one solve (ncu launch list, "
+                    "frac": achieved / peak,
+                    "traffic": ncu_kernel_step_traffic("tiled_solve", "k_tile_middle_wide"),
+                    "traffic_scope": "DRAM read+write bytes of all middle launches of one solve (ncu launch list, "
                                      "profiles/ncu_summary.json tiled_solve)",
-                    "kernel": "tiled fill (k_tile_middle + k_sub_product + k_sub_leaf, all tile diagonals)",
-                    "peak_model": "148 SMs x sm_max_mhz x 21.33 transitions/clk/SM (fp64 pipe: DADD 64 "
-                                  "lanes/clk + DSETP 32 lanes/clk per SM, measured scripts/microbench_minplus.cu)",
-                    "launches_per_step": fill_launches, "fill_ms_per_step": fill_avg_ms,
-                    "hbm_wavefront_equiv_frac": alg_bytes_wavefront(L, S) / (fill_avg_ms / 1e3) / 1e9
-                    / float(peaks["hbm_gbs"])}
+                    "kernel": "k_tile_middle_wide (pruned middle: fp32 lower-bound filter, exact fp64 recompute)",
+                    "peak_model": "148 SMs x sm_max_mhz x 64 candidates/clk/SM (one FSETP per candidate on the "
+                                  "ALU pipe)",
+                    "transitions_per_step": tm, "middle_ms_per_step": mid_avg_ms,
+                    "middle_launches_per_step": mid_launches,
+                    "middle_share_of_fill": mid_avg_ms / fill_avg_ms,
+                    "fill": {"achieved": fill_ach, "peak": fill_peak, "frac": fill_ach / fill_peak,
+                             "unit": "Gtransitions/s", "ms_per_step": fill_avg_ms, "launches_per_step": fill_launches,
+                             "peak_model": "148 SMs x sm_max_mhz x 21.33 transitions/clk/SM (exact fp64 evaluation: "
+                                           "DADD 64 + DSETP 32 lanes/clk/SM, scripts/microbench_minplus.cu)",
+                             "traffic": ncu_step_traffic("tiled_solve"),
+                             "hbm_wavefront_equiv_frac": alg_bytes_wavefront(L, S) / (fill_avg_ms / 1e3) / 1e9
+                             / float(peaks["hbm_gbs"])}}
     else:
         b_alg = alg_bytes_wavefront(L, S)
         achieved = b_alg / (fill_avg_ms / 1e3) / 1e9  # GB/s, fill phase = all K2 launches

@@ -219,6 +219,8 @@ typedef struct {
     double reconstruct_ms; /* Algorithm 2 walk */
     int32_t fill_launches; /* kernels launched for the fill */
     int32_t total_launches;/* kernels launched by the solve */
+    double middle_ms;      /* tiled fill: the middle-kernel launches alone (events on the launch stream) */
+    int32_t middle_launches;
 } rotor_timings;
 int rotor_last_timings(rotor_timings *out);
 

@@ -55,6 +55,7 @@ class rotor_timings(ctypes.Structure):
     _fields_ = [
         ("pre_ms", ctypes.c_double), ("fill_ms", ctypes.c_double), ("reconstruct_ms", ctypes.c_double),
         ("fill_launches", ctypes.c_int32), ("total_launches", ctypes.c_int32),
+        ("middle_ms", ctypes.c_double), ("middle_launches", ctypes.c_int32),
     ]
 
 
@@ -251,7 +252,8 @@ def last_timings() -> dict:
     t = rotor_timings()
     _check(_lib.rotor_last_timings(_c.byref(t)))
     return dict(pre_ms=t.pre_ms, fill_ms=t.fill_ms, reconstruct_ms=t.reconstruct_ms,
-                fill_launches=t.fill_launches, total_launches=t.total_launches)
+                fill_launches=t.fill_launches, total_launches=t.total_launches,
+                middle_ms=t.middle_ms, middle_launches=t.middle_launches)
 
 
 def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=None, **opts):

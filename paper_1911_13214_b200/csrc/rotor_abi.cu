@@ -10,6 +10,7 @@
 #include <map>
 #include <mutex>
 #include <numeric>
+#include <vector>
 #include <string>
 #include <vector>
 
@@ -173,6 +174,8 @@ struct LastSolve {
     bool profiled = false;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     int fill_launches = 0, total_launches = 0;
+    std::vector<cudaEvent_t> mid_ev;  // pairs around the tiled fill's middle launches
+    int mid_n = 0;
 };
 thread_local LastSolve g_last;
 
@@ -250,7 +253,17 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
     if (o.profile) CK(cudaEventRecord(g_last.ev[1], st));
     int fill = 0;
     if (y.has_A) {
-        fill = rotor::launch_fill_tiled(p, st);
+        g_last.mid_n = 0;
+        int cap = 0;
+        if (o.profile) {
+            cap = rotor::tiled_nb(y.n);
+            while ((int)g_last.mid_ev.size() < 2 * cap) {
+                cudaEvent_t e;
+                CK(cudaEventCreate(&e));
+                g_last.mid_ev.push_back(e);
+            }
+        }
+        fill = rotor::launch_fill_tiled(p, st, cap ? g_last.mid_ev.data() : nullptr, cap, &g_last.mid_n);
         if (fill < 0) {
             cudaError_t e = cudaGetLastError();
             return fail(ROTOR_EDEVICE, "tiled fill launch failed: %s", cudaGetErrorString(e));
@@ -705,6 +718,14 @@ int rotor_last_timings(rotor_timings *out) {
     out->reconstruct_ms = c;
     out->fill_launches = g_last.fill_launches;
     out->total_launches = g_last.total_launches;
+    double mid = 0;
+    for (int i = 0; i < g_last.mid_n; i++) {
+        float x = 0;
+        CK(cudaEventElapsedTime(&x, g_last.mid_ev[2 * i], g_last.mid_ev[2 * i + 1]));
+        mid += x;
+    }
+    out->middle_ms = mid;
+    out->middle_launches = g_last.mid_n;
     return ROTOR_OK;
 }
 

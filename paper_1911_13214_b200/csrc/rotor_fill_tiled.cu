@@ -271,590 +271,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Pruned middle (default): the same partial minimum with most of the fp64
-// candidates skipped by an exact fp32 lower-bound filter.
-//
-// For a candidate v = fl64(a + b) with a, b >= 0 (or +inf), the fp32 value
-//     lb = fadd_rd( cvt_rd(a), cvt_rd(b) )
-// satisfies lb <= a + b, and since lb is also an fp64 number and rounding is
-// monotone, lb <= fl64(a + b) = v.  So if the minimum of lb over a chunk of KC
-// splits is >= the running fp64 minimum acc of a cell, no candidate of the
-// chunk can lower acc, and skipping them leaves acc bit-identical (the min is
-// exact; ties do not matter because the fill keeps values, not argmins).
-// cvt.rm maps +inf to +inf and finite values above FLT_MAX to FLT_MAX, so the
-// bound holds for every input.  Cost per candidate: FADD.RM + FMNMX on the
-// fp32/ALU pipes instead of DADD + DSETP (half rate) + 2 SEL; a warp runs the
-// exact fp64 chunk only when one of its 16 m x 32 cells can improve (about
-// one chunk in eight at config 4 in ascending s' order: the running minimum
-// settles early, DESIGN 5.2).
-// The fp32 copies of a stage are made once per CTA (each warp converts 1/16
-// of the stage) and published through a per-stage mbarrier.
-// ---------------------------------------------------------------------------
-template <int KC_, int STAGES_>
-struct PrunedRing {
-    static constexpr int KC = KC_, STAGES = STAGES_;
-    static constexpr int A_ST = KC * TB * TM, B_ST = KC * TB * TMB;  // doubles per stage
-    static constexpr size_t bytes = (size_t)STAGES * (A_ST + B_ST) * 12  // fp64 boxes + fp32 copies
-                                    + 3 * STAGES * 8 + STAGES * KC * 4 + 64;
-};
-
-template <int KC_, int STAGES_>
-__global__ void __launch_bounds__(THREADS, 1)
-    k_tile_middle_pruned(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
-                         Problem p, int delta, int tile_lo, int n_tiles) {
-    using R = PrunedRing<KC_, STAGES_>;
-    constexpr int KC = R::KC, STAGES = R::STAGES, A_ST = R::A_ST, B_ST = R::B_ST;
-    extern __shared__ __align__(1024) double smem[];
-    double *As = smem;                                         // [STAGES][KC][TB][TM]
-    double *Bs = As + STAGES * A_ST;                           // [STAGES][KC][TB][TMB]
-    float *Af = reinterpret_cast<float *>(Bs + STAGES * B_ST);  // fp32 round-down copies, same layout
-    float *Bf = Af + STAGES * A_ST;
-    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + STAGES * B_ST);
-    uint64_t *empty = full + STAGES;
-    uint64_t *conv = empty + STAGES;                     // fp32 copy of stage complete (16 warp arrivals)
-    int *soff = reinterpret_cast<int *>(conv + STAGES);  // [STAGES][KC]
-    int *wx_s = soff + STAGES * KC;
-
-    const int n = p.n;
-    const int n_mc = (p.S + 1 + TM - 1) / TM;
-    const int n_items = n_tiles * n_mc;
-    if ((int)blockIdx.x >= n_items) return;
-    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int iters = (delta - 1) * TB / KC;
-    const int total = my_items * iters;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31, warp = tid >> 5;
-    const int *wxp = p.wx;
-    if (n <= WX_SMEM_MAX) {
-        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
-        wxp = wx_s;
-    }
-
-    auto issue = [&](int gi) {  // as k_tile_middle
-        const int st = gi % STAGES;
-        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
-        const int I = tile_lo + item / n_mc, J = I + delta;
-        const int i0 = I * TB + 1, j0 = J * TB + 1, m0 = (item % n_mc) * TM;
-        const int sp0 = i0 + TB + (gi % iters) * KC;
-        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 1;
-        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 8));
-        for (int k = 0; k < KC; k++)
-            tma_load_2d(As + st * A_ST + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
-        for (int k = 0; k < KC; k++) {
-            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
-            tma_load_2d(Bs + st * B_ST + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp0 + k, j0), &full[st]);
-        }
-    };
-
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CONSUMERS / 32);
-            mbar_init(&conv[s], CONSUMERS / 32);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    constexpr int PRODUCER = CONSUMERS - 32;
-    if (tid == PRODUCER)
-        for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);
-
-    const int mi = tid & 15;
-    const int g = tid >> 4;
-    const int sg = g / (TB / RT), tg = g % (TB / RT);
-    constexpr int PAIRS = (A_ST + B_ST) / 2;  // double2 per stage
-    for (int kl = 0; kl < my_items; kl++) {
-        double acc[RS][RT];
-#pragma unroll
-        for (int i = 0; i < RS; i++)
-#pragma unroll
-            for (int j = 0; j < RT; j++) acc[i][j] = INFINITY;
-
-        for (int it = 0; it < iters; it++) {
-            const int gi = kl * iters + it;
-            const int st = gi % STAGES;
-            const uint32_t par = (uint32_t)((gi / STAGES) & 1);
-            mbar_wait(&full[st], par);
-            {  // this warp's share of the stage's fp32 copy
-                const double2 *a2 = reinterpret_cast<const double2 *>(As + st * A_ST);
-                const double2 *b2 = reinterpret_cast<const double2 *>(Bs + st * B_ST);
-                float2 *af2 = reinterpret_cast<float2 *>(Af + st * A_ST);
-                float2 *bf2 = reinterpret_cast<float2 *>(Bf + st * B_ST);
-                for (int q = tid; q < PAIRS; q += THREADS) {
-                    const bool isA = q < A_ST / 2;
-                    const double2 v = isA ? a2[q] : b2[q - A_ST / 2];
-                    const float2 f = make_float2(__double2float_rd(v.x), __double2float_rd(v.y));
-                    if (isA) af2[q] = f; else bf2[q - A_ST / 2] = f;
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&conv[st]);
-            }
-            mbar_wait(&conv[st], par);
-            // filter: per cell the minimum lower bound over the KC splits
-            float mn[RS][RT];
-            {
-                const float *a_f = Af + st * A_ST + (sg * RS) * TM + mi;
-                const float *b_f = Bf + st * B_ST + (tg * RT) * TMB + mi;
-#pragma unroll
-                for (int k = 0; k < KC; k++) {
-                    float a[RS], b[RT];
-                    const float *bk = b_f + k * TB * TMB + soff[st * KC + k];
-#pragma unroll
-                    for (int i = 0; i < RS; i++) a[i] = a_f[k * TB * TM + i * TM];
-#pragma unroll
-                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
-#pragma unroll
-                    for (int i = 0; i < RS; i++)
-#pragma unroll
-                        for (int j = 0; j < RT; j++) {
-                            const float v = __fadd_rd(a[i], b[j]);
-                            mn[i][j] = k == 0 ? v : fminf(mn[i][j], v);
-                        }
-                }
-            }
-            bool need = false;
-#pragma unroll
-            for (int i = 0; i < RS; i++)
-#pragma unroll
-                for (int j = 0; j < RT; j++) need |= (double)mn[i][j] < acc[i][j];
-            if (__any_sync(0xffffffffu, need)) {  // exact fp64 chunk (as k_tile_middle)
-                const double *a_s = As + st * A_ST + (sg * RS) * TM + mi;
-                const double *b_s = Bs + st * B_ST + (tg * RT) * TMB + mi;
-#pragma unroll
-                for (int k = 0; k < KC; k++) {
-                    double a[RS], b[RT];
-                    const double *bk = b_s + k * TB * TMB + soff[st * KC + k];
-#pragma unroll
-                    for (int i = 0; i < RS; i++) a[i] = a_s[k * TB * TM + i * TM];
-#pragma unroll
-                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
-#pragma unroll
-                    for (int i = 0; i < RS; i++)
-#pragma unroll
-                        for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            if (tid == PRODUCER && gi + STAGES < total) {
-                mbar_wait(&empty[st], par);
-                issue(gi + STAGES);
-            }
-        }
-
-        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
-        const int I = tile_lo + item / n_mc, J = I + delta;
-        const int i0 = I * TB + 1, j0 = J * TB + 1;
-        const int m = (item % n_mc) * TM + mi;
-        if (m <= p.S) {
-#pragma unroll
-            for (int i = 0; i < RS; i++) {
-                const int s = i0 + sg * RS + i;
-#pragma unroll
-                for (int j = 0; j < RT; j++) {
-                    const int t = j0 + tg * RT + j;
-                    if (t <= n) p.C[cell_index(n, s, t) * p.pitch + m] = acc[i][j];
-                }
-            }
-        }
-    }
-}
-// Decoupled variant: the fp64 boxes land in a 2-slot TMA ring that is
-// released as soon as every warp has converted its share into a separate
-// 2-slot fp32 ring; a warp converts chunk gi+1 before filtering chunk gi, so a
-// warp that lags by up to one chunk (an exact pass) does not stall the others,
-// and both fp64 slots are in flight while a chunk is filtered.  The rare exact
-// chunk reads its fp64 operands from global memory (L2: the TMA just fetched
-// them).  Same values as the TMA boxes on every non-gated cell (a C operand
-// at m - wx < 0 is +inf there; below -kPad the boxes are clamped, but those
-// cells are gated, DESIGN Q6).
-struct Pruned2Ring {
-    static constexpr int KC = 8, S64 = 2, S32 = 2;
-    static constexpr int A_ST = KC * TB * TM, B_ST = KC * TB * TMB;
-    static constexpr size_t bytes = (size_t)S64 * (A_ST + B_ST) * 8 + (size_t)S32 * (A_ST + B_ST) * 4 +
-                                    (2 * S64 + 2 * S32) * 8 + S32 * KC * 4 + 64;
-};
-
-__global__ void __launch_bounds__(THREADS, 1)
-    k_tile_middle_pruned2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
-                          Problem p, int delta, int tile_lo, int n_tiles) {
-    using R = Pruned2Ring;
-    constexpr int KC = R::KC, S64 = R::S64, S32 = R::S32, A_ST = R::A_ST, B_ST = R::B_ST;
-    extern __shared__ __align__(1024) double smem[];
-    double *As = smem;                                         // [S64][KC][TB][TM]
-    double *Bs = As + S64 * A_ST;                              // [S64][KC][TB][TMB]
-    float *Af = reinterpret_cast<float *>(Bs + S64 * B_ST);    // [S32][KC][TB][TM]
-    float *Bf = Af + S32 * A_ST;                               // [S32][KC][TB][TMB]
-    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + S32 * B_ST);  // fp64 slot landed (TMA tx)
-    uint64_t *empty = full + S64;                              // fp64 slot converted by all 16 warps
-    uint64_t *conv = empty + S64;                              // fp32 slot ready (16 warps)
-    uint64_t *free32 = conv + S32;                             // fp32 slot consumed (16 warps)
-    int *soff = reinterpret_cast<int *>(free32 + S32);         // [S32][KC] box column offsets
-    int *wx_s = soff + S32 * KC;
-
-    const int n = p.n;
-    const int n_mc = (p.S + 1 + TM - 1) / TM;
-    const int n_items = n_tiles * n_mc;
-    if ((int)blockIdx.x >= n_items) return;
-    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int iters = (delta - 1) * TB / KC;
-    const int total = my_items * iters;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int *wxp = p.wx;
-    if (n <= WX_SMEM_MAX) {
-        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
-        wxp = wx_s;
-    }
-    auto coords = [&](int gi, int &i0, int &j0, int &m0, int &sp0) {
-        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
-        const int I = tile_lo + item / n_mc, J = I + delta;
-        i0 = I * TB + 1;
-        j0 = J * TB + 1;
-        m0 = (item % n_mc) * TM;
-        sp0 = i0 + TB + (gi % iters) * KC;
-    };
-    auto issue = [&](int gi) {
-        const int st = gi % S64;
-        int i0, j0, m0, sp0;
-        coords(gi, i0, j0, m0, sp0);
-        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 8));
-        for (int k = 0; k < KC; k++)
-            tma_load_2d(As + st * A_ST + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
-        for (int k = 0; k < KC; k++) {
-            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
-            tma_load_2d(Bs + st * B_ST + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp0 + k, j0), &full[st]);
-        }
-    };
-    if (tid == 0) {
-        for (int s = 0; s < S64; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CONSUMERS / 32);
-        }
-        for (int s = 0; s < S32; s++) {
-            mbar_init(&conv[s], CONSUMERS / 32);
-            mbar_init(&free32[s], CONSUMERS / 32);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    constexpr int PRODUCER = CONSUMERS - 32;
-    if (tid == PRODUCER)
-        for (int gi = 0; gi < S64 && gi < total; gi++) issue(gi);
-
-    const int warp = tid >> 5;
-    // chunk gi: fp64 slot gi % S64 -> fp32 slot gi % S32 (this warp's 1/16 share)
-    auto convert = [&](int gi) {
-        const int s64 = gi % S64, s32 = gi % S32;
-        if (gi >= S32) mbar_wait(&free32[s32], (uint32_t)(((gi - S32) / S32) & 1));  // chunk gi-S32 consumed
-        mbar_wait(&full[s64], (uint32_t)((gi / S64) & 1));
-        if (lane == 0) {  // box column offsets of this chunk (read by the filter after conv)
-            if (warp == 0) {
-                int i0, j0, m0, sp0;
-                coords(gi, i0, j0, m0, sp0);
-                for (int k = 0; k < KC; k++) soff[s32 * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 1;
-            }
-        }
-        constexpr int PA = A_ST / 2, PT = (A_ST + B_ST) / 2, PER = PT / (CONSUMERS / 32);
-        const double2 *a2 = reinterpret_cast<const double2 *>(As + s64 * A_ST);
-        const double2 *b2 = reinterpret_cast<const double2 *>(Bs + s64 * B_ST);
-        float2 *af2 = reinterpret_cast<float2 *>(Af + s32 * A_ST);
-        float2 *bf2 = reinterpret_cast<float2 *>(Bf + s32 * B_ST);
-        static_assert(PT % (CONSUMERS / 32) == 0, "even conversion shares");
-#pragma unroll 3
-        for (int q = warp * PER + lane; q < (warp + 1) * PER; q += 32) {
-            const double2 v = q < PA ? a2[q] : b2[q - PA];
-            const float2 f = make_float2(__double2float_rd(v.x), __double2float_rd(v.y));
-            if (q < PA) af2[q] = f; else bf2[q - PA] = f;
-        }
-        __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(&empty[s64]);
-            mbar_arrive(&conv[s32]);
-        }
-    };
-
-    const int mi = tid & 15;
-    const int g = tid >> 4;
-    const int sg = g / (TB / RT), tg = g % (TB / RT);
-    // once every warp has converted chunk c, its fp64 slot takes chunk c + S64
-    auto refill = [&](int c) {
-        if (tid == PRODUCER && c + S64 < total) {
-            mbar_wait(&empty[c % S64], (uint32_t)((c / S64) & 1));
-            issue(c + S64);
-        }
-    };
-    if (total > 0) {
-        convert(0);
-        refill(0);
-    }
-    for (int kl = 0; kl < my_items; kl++) {
-        double acc[RS][RT];
-#pragma unroll
-        for (int i = 0; i < RS; i++)
-#pragma unroll
-            for (int j = 0; j < RT; j++) acc[i][j] = INFINITY;
-        for (int it = 0; it < iters; it++) {
-            const int gi = kl * iters + it;
-            if (gi + 1 < total) {
-                convert(gi + 1);
-                refill(gi + 1);
-            }
-            const int s32 = gi % S32;
-            mbar_wait(&conv[s32], (uint32_t)((gi / S32) & 1));
-            float mn[RS][RT];
-            {
-                const float *a_f = Af + s32 * A_ST + (sg * RS) * TM + mi;
-                const float *b_f = Bf + s32 * B_ST + (tg * RT) * TMB + mi;
-#pragma unroll
-                for (int k = 0; k < KC; k++) {
-                    float a[RS], b[RT];
-                    const float *bk = b_f + k * TB * TMB + soff[s32 * KC + k];
-#pragma unroll
-                    for (int i = 0; i < RS; i++) a[i] = a_f[k * TB * TM + i * TM];
-#pragma unroll
-                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
-#pragma unroll
-                    for (int i = 0; i < RS; i++)
-#pragma unroll
-                        for (int j = 0; j < RT; j++) {
-                            const float v = __fadd_rd(a[i], b[j]);
-                            mn[i][j] = k == 0 ? v : fminf(mn[i][j], v);
-                        }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&free32[s32]);
-            bool need = false;
-#pragma unroll
-            for (int i = 0; i < RS; i++)
-#pragma unroll
-                for (int j = 0; j < RT; j++) need |= (double)mn[i][j] < acc[i][j];
-            if (__any_sync(0xffffffffu, need)) {  // exact fp64 chunk, operands from global memory
-                int i0, j0, m0, sp0;
-                coords(gi, i0, j0, m0, sp0);
-                const int m = min(m0 + mi, p.S);
-                const int s_0 = i0 + sg * RS, t_0 = j0 + tg * RT;
-#pragma unroll 2
-                for (int k = 0; k < KC; k++) {
-                    const int sp = sp0 + k;
-                    const int mm = m - wxp[sp - 1];
-                    double a[RS], b[RT];
-                    const double *ap = p.A + a_index(s_0, sp - 1) * p.pitch + m;
-#pragma unroll
-                    for (int i = 0; i < RS; i++) a[i] = __ldcg(ap + (int64_t)i * p.pitch);
-                    const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
-#pragma unroll
-                    for (int j = 0; j < RT; j++)
-                        b[j] = (mm >= 0 && t_0 + j <= n) ? __ldcg(bp + (int64_t)j * p.pitch) : INFINITY;
-#pragma unroll
-                    for (int i = 0; i < RS; i++)
-#pragma unroll
-                        for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
-                }
-            }
-        }
-        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
-        const int I = tile_lo + item / n_mc, J = I + delta;
-        const int i0 = I * TB + 1, j0 = J * TB + 1;
-        const int m = (item % n_mc) * TM + mi;
-        if (m <= p.S) {
-#pragma unroll
-            for (int i = 0; i < RS; i++) {
-                const int s = i0 + sg * RS + i;
-#pragma unroll
-                for (int j = 0; j < RT; j++) {
-                    const int t = j0 + tg * RT + j;
-                    if (t <= n) p.C[cell_index(n, s, t) * p.pitch + m] = acc[i][j];
-                }
-            }
-        }
-    }
-}
-
-// Variant 3: fp64 boxes in a 5-slot TMA ring of KC = 4 splits (three slots in
-// flight while one is filtered), their fp32 copies in a separate 2-slot ring;
-// a warp converts its share of chunk gi+1 before filtering chunk gi (one chunk
-// of slack between warps); per cell an fp32 upper bound of the running
-// minimum (bestf = cvt_ru(acc)) so the filter is FADD.RM + FSETP.OR per
-// candidate with no per-chunk check; the exact pass reads the fp64 slot.
-struct Pruned3Ring {
-    static constexpr int KC = 4, S64 = 5, S32 = 2;
-    static constexpr int A_ST = KC * TB * TM, B_ST = KC * TB * TMB;
-    static constexpr size_t bytes = (size_t)S64 * (A_ST + B_ST) * 8 + (size_t)S32 * (A_ST + B_ST) * 4 +
-                                    (2 * S64 + 2 * S32) * 8 + (S64 + S32) * KC * 4 + 64;
-};
-
-__global__ void __launch_bounds__(THREADS, 1)
-    k_tile_middle_pruned3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC,
-                          Problem p, int delta, int tile_lo, int n_tiles) {
-    using R = Pruned3Ring;
-    constexpr int KC = R::KC, S64 = R::S64, S32 = R::S32, A_ST = R::A_ST, B_ST = R::B_ST;
-    extern __shared__ __align__(1024) double smem[];
-    double *As = smem;                                         // [S64][KC][TB][TM]
-    double *Bs = As + S64 * A_ST;                              // [S64][KC][TB][TMB]
-    float *Af = reinterpret_cast<float *>(Bs + S64 * B_ST);    // [S32][KC][TB][TM]
-    float *Bf = Af + S32 * A_ST;                               // [S32][KC][TB][TMB]
-    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + S32 * B_ST);  // fp64 slot landed (TMA tx)
-    uint64_t *empty = full + S64;                              // fp64 slot done (16 warps)
-    uint64_t *conv = empty + S64;                              // fp32 slot ready (16 warps)
-    uint64_t *free32 = conv + S32;                             // fp32 slot consumed (16 warps)
-    int *soff = reinterpret_cast<int *>(free32 + S32);         // [S64][KC] box column offsets
-    int *wx_s = soff + (S64 + S32) * KC;
-
-    const int n = p.n;
-    const int n_mc = (p.S + 1 + TM - 1) / TM;
-    const int n_items = n_tiles * n_mc;
-    if ((int)blockIdx.x >= n_items) return;
-    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int iters = (delta - 1) * TB / KC;
-    const int total = my_items * iters;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int *wxp = p.wx;
-    if (n <= WX_SMEM_MAX) {
-        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
-        wxp = wx_s;
-    }
-    auto issue = [&](int gi) {
-        const int st = gi % S64;
-        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
-        const int I = tile_lo + item / n_mc, J = I + delta;
-        const int i0 = I * TB + 1, j0 = J * TB + 1, m0 = (item % n_mc) * TM;
-        const int sp0 = i0 + TB + (gi % iters) * KC;
-        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 1;
-        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 8));
-        for (int k = 0; k < KC; k++)
-            tma_load_2d(As + st * A_ST + k * TB * TM, &tmA, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
-        for (int k = 0; k < KC; k++) {
-            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
-            tma_load_2d(Bs + st * B_ST + k * TB * TMB, &tmC, c0 & ~1, (int)cell_index(n, sp0 + k, j0), &full[st]);
-        }
-    };
-    if (tid == 0) {
-        for (int s = 0; s < S64; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CONSUMERS / 32);
-        }
-        for (int s = 0; s < S32; s++) {
-            mbar_init(&conv[s], CONSUMERS / 32);
-            mbar_init(&free32[s], CONSUMERS / 32);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    constexpr int PRODUCER = CONSUMERS - 32;
-    if (tid == PRODUCER)
-        for (int gi = 0; gi < S64 && gi < total; gi++) issue(gi);
-
-    const int warp = tid >> 5;
-    auto convert = [&](int gi) {  // this warp's 1/16 share of chunk gi: fp64 slot -> fp32 slot
-        const int s64 = gi % S64, s32 = gi % S32;
-        if (gi >= S32) mbar_wait(&free32[s32], (uint32_t)(((gi - S32) / S32) & 1));
-        mbar_wait(&full[s64], (uint32_t)((gi / S64) & 1));
-        constexpr int PA = A_ST / 2, PT = (A_ST + B_ST) / 2, PER = PT / (CONSUMERS / 32);
-        static_assert(PT % (CONSUMERS / 32) == 0, "even conversion shares");
-        const double2 *a2 = reinterpret_cast<const double2 *>(As + s64 * A_ST);
-        const double2 *b2 = reinterpret_cast<const double2 *>(Bs + s64 * B_ST);
-        float2 *af2 = reinterpret_cast<float2 *>(Af + s32 * A_ST);
-        float2 *bf2 = reinterpret_cast<float2 *>(Bf + s32 * B_ST);
-#pragma unroll
-        for (int q = warp * PER + lane; q < (warp + 1) * PER; q += 32) {
-            const double2 v = q < PA ? a2[q] : b2[q - PA];
-            const float2 f = make_float2(__double2float_rd(v.x), __double2float_rd(v.y));
-            if (q < PA) af2[q] = f; else bf2[q - PA] = f;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&conv[s32]);
-    };
-
-    const int mi = tid & 15;
-    const int g = tid >> 4;
-    const int sg = g / (TB / RT), tg = g % (TB / RT);
-    if (total > 0) convert(0);
-    for (int kl = 0; kl < my_items; kl++) {
-        double acc[RS][RT];
-        float bestf[RS][RT];  // fp32 upper bound of acc
-#pragma unroll
-        for (int i = 0; i < RS; i++)
-#pragma unroll
-            for (int j = 0; j < RT; j++) {
-                acc[i][j] = INFINITY;
-                bestf[i][j] = INFINITY;
-            }
-        for (int it = 0; it < iters; it++) {
-            const int gi = kl * iters + it;
-            if (gi + 1 < total) convert(gi + 1);
-            const int s32 = gi % S32, s64 = gi % S64;
-            mbar_wait(&conv[s32], (uint32_t)((gi / S32) & 1));
-            bool need = false;
-            {
-                const float *a_f = Af + s32 * A_ST + (sg * RS) * TM + mi;
-                const float *b_f = Bf + s32 * B_ST + (tg * RT) * TMB + mi;
-#pragma unroll
-                for (int k = 0; k < KC; k++) {
-                    float a[RS], b[RT];
-                    const float *bk = b_f + k * TB * TMB + soff[s64 * KC + k];
-#pragma unroll
-                    for (int i = 0; i < RS; i++) a[i] = a_f[k * TB * TM + i * TM];
-#pragma unroll
-                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
-#pragma unroll
-                    for (int i = 0; i < RS; i++)
-#pragma unroll
-                        for (int j = 0; j < RT; j++) need |= __fadd_rd(a[i], b[j]) < bestf[i][j];
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&free32[s32]);
-            if (__any_sync(0xffffffffu, need)) {  // exact fp64 chunk from the fp64 slot
-                const double *a_s = As + s64 * A_ST + (sg * RS) * TM + mi;
-                const double *b_s = Bs + s64 * B_ST + (tg * RT) * TMB + mi;
-#pragma unroll
-                for (int k = 0; k < KC; k++) {
-                    double a[RS], b[RT];
-                    const double *bk = b_s + k * TB * TMB + soff[s64 * KC + k];
-#pragma unroll
-                    for (int i = 0; i < RS; i++) a[i] = a_s[k * TB * TM + i * TM];
-#pragma unroll
-                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB];
-#pragma unroll
-                    for (int i = 0; i < RS; i++)
-#pragma unroll
-                        for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
-                }
-#pragma unroll
-                for (int i = 0; i < RS; i++)
-#pragma unroll
-                    for (int j = 0; j < RT; j++) bestf[i][j] = __double2float_ru(acc[i][j]);
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s64]);
-            if (tid == PRODUCER && gi + S64 < total) {
-                mbar_wait(&empty[s64], (uint32_t)((gi / S64) & 1));
-                issue(gi + S64);
-            }
-        }
-        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
-        const int I = tile_lo + item / n_mc, J = I + delta;
-        const int i0 = I * TB + 1, j0 = J * TB + 1;
-        const int m = (item % n_mc) * TM + mi;
-        if (m <= p.S) {
-#pragma unroll
-            for (int i = 0; i < RS; i++) {
-                const int s = i0 + sg * RS + i;
-#pragma unroll
-                for (int j = 0; j < RT; j++) {
-                    const int t = j0 + tg * RT + j;
-                    if (t <= n) p.C[cell_index(n, s, t) * p.pitch + m] = acc[i][j];
-                }
-            }
-        }
-    }
-}
-
-// ---------------------------------------------------------------------------
-// Pruned middle on the fp32 shadow tables (default).  The leaf kernels store,
+// Pruned middle on the fp32 shadow tables (16-m items; the wide variant below
+// is the default).  The leaf kernels store,
 // with every final C and A value, its round-down fp32 copy (store_final_*), so
 // the TMA ring carries only fp32 boxes (half the bytes of the fp64 boxes: six
 // 36 KB stages, five in flight) and there is nothing to convert on chip.
@@ -942,14 +360,25 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int sg = g / (TB / RT), tg = g % (TB / RT);
     for (int kl = 0; kl < my_items; kl++) {
         double acc[RS][RT];
-        float bestf[RS][RT];  // cvt_ru(acc) >= acc
+        // bestf = cvt_ru(acc) >= acc; -inf (never passes the filter) on the
+        // cells whose partial is never used: gated (m < m_null(s,t), P:726 —
+        // the C operand there can come from a clamped box or a pad, DESIGN
+        // Q6), t > n, and m > S
+        float bestf[RS][RT];
+        {
+            const int item = (int)blockIdx.x + kl * (int)gridDim.x;
+            const int I = tile_lo + item / n_mc, J = I + delta;
+            const int s_0 = I * TB + 1 + sg * RS, t_0 = J * TB + 1 + tg * RT;
+            const int m = (item % n_mc) * TM + mi;
 #pragma unroll
-        for (int i = 0; i < RS; i++)
+            for (int i = 0; i < RS; i++)
 #pragma unroll
-            for (int j = 0; j < RT; j++) {
-                acc[i][j] = INFINITY;
-                bestf[i][j] = INFINITY;
-            }
+                for (int j = 0; j < RT; j++) {
+                    acc[i][j] = INFINITY;
+                    const int t = t_0 + j;
+                    bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + i, t)) ? INFINITY : -INFINITY;
+                }
+        }
         for (int it = 0; it < iters; it++) {
             const int gi = kl * iters + it;
             const int st = gi % STAGES;
@@ -1024,10 +453,177 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
 }
 
-// (the wx copy sized by WX_SMEM_MAX leaves 1 KB of the 227 KB spare)
-static_assert(PrunedRing<8, 2>::bytes <= SMEM_BYTES + 512 && PrunedRing<4, 4>::bytes <= SMEM_BYTES + 512 &&
-                  Pruned2Ring::bytes <= SMEM_BYTES + 512 && Pruned3Ring::bytes <= SMEM_BYTES + 512,
-              "pruned rings fit the exact ring's allocation");
+// ---------------------------------------------------------------------------
+// Wide pruned middle: items of 32 s x 32 t x 32 m; a warp = 32 consecutive m
+// of one 8 x 8 (s,t) register tile.  The fp32 boxes have 128-byte (A) and
+// 144-byte (C) rows — twice the row length of the 16-m items, half the row
+// requests per byte — and each lane keeps only bestf for its 64 cells in
+// registers; the exact fp64 running minimum lives in the partial rows of C
+// in global memory (the middle kernel is their first writer), touched only
+// by the rare exact passes, which recompute just the splits whose filter
+// fired (per-split mask OR-reduced over the warp).
+// ---------------------------------------------------------------------------
+constexpr int TMW = 32, TMBW = TMW + 4, RW = 8;
+struct WideRing {
+    static constexpr int KC = 4, STAGES = 6;
+    static constexpr int A_ST = KC * TB * TMW, B_ST = KC * TB * TMBW;  // floats per stage
+    static constexpr size_t bytes = (size_t)STAGES * (A_ST + B_ST) * 4 + 2 * STAGES * 8 + STAGES * KC * 4 + 64;
+};
+constexpr int WIDE_WX_MAX = (int)((227 * 1024 - WideRing::bytes) / 4);
+static_assert((TB / RW) * (TB / RW) * TMW == THREADS, "one lane per (m, 8x8 tile)");
+
+__global__ void __launch_bounds__(THREADS, 1)
+    k_tile_middle_wide(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmC32,
+                       Problem p, int delta, int tile_lo, int n_tiles) {
+    using R = WideRing;
+    constexpr int KC = R::KC, STAGES = R::STAGES, A_ST = R::A_ST, B_ST = R::B_ST;
+    extern __shared__ __align__(1024) float fsm[];
+    float *Af = fsm;                 // [STAGES][KC][TB s][TMW]
+    float *Bf = Af + STAGES * A_ST;  // [STAGES][KC][TB t][TMBW]
+    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + STAGES * B_ST);
+    uint64_t *empty = full + STAGES;
+    int *soff = reinterpret_cast<int *>(empty + STAGES);  // [STAGES][KC]
+    int *wx_s = soff + STAGES * KC;
+
+    const int n = p.n;
+    const int n_mc = (p.S + 1 + TMW - 1) / TMW;
+    const int n_items = n_tiles * n_mc;
+    if ((int)blockIdx.x >= n_items) return;
+    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int iters = (delta - 1) * TB / KC;
+    const int total = my_items * iters;
+    const int tid = threadIdx.x;
+    const int lane = tid & 31, warp = tid >> 5;
+    const int *wxp = p.wx;
+    if (n <= WIDE_WX_MAX) {
+        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
+        wxp = wx_s;
+    }
+    auto coords = [&](int gi, int &i0, int &j0, int &m0, int &sp0) {
+        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        i0 = I * TB + 1;
+        j0 = J * TB + 1;
+        m0 = (item % n_mc) * TMW;
+        sp0 = i0 + TB + (gi % iters) * KC;
+    };
+    auto issue = [&](int gi) {
+        const int st = gi % STAGES;
+        int i0, j0, m0, sp0;
+        coords(gi, i0, j0, m0, sp0);
+        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 3;
+        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 4));
+        for (int k = 0; k < KC; k++)
+            tma_load_2d(Af + st * A_ST + k * TB * TMW, &tmA32, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
+        for (int k = 0; k < KC; k++) {
+            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
+            tma_load_2d(Bf + st * B_ST + k * TB * TMBW, &tmC32, c0 & ~3, (int)cell_index(n, sp0 + k, j0),
+                        &full[st]);
+        }
+    };
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], CONSUMERS / 32);
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    constexpr int PRODUCER = CONSUMERS - 32;
+    if (tid == PRODUCER)
+        for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);
+
+    const int sg = warp / (TB / RW), tg = warp % (TB / RW);
+    for (int kl = 0; kl < my_items; kl++) {
+        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
+        const int I = tile_lo + item / n_mc, J = I + delta;
+        const int s_0 = I * TB + 1 + sg * RW, t_0 = J * TB + 1 + tg * RW;
+        const int m = (item % n_mc) * TMW + lane;
+        const int mc = min(m, p.S);
+        // bestf >= the exact partial minimum; -inf on cells whose partial is
+        // never used (gated: m < m_null(s,t), DESIGN Q6; t > n; m > S)
+        float bestf[RW][RW];
+#pragma unroll
+        for (int i = 0; i < RW; i++)
+#pragma unroll
+            for (int j = 0; j < RW; j++) {
+                const int t = t_0 + j;
+                bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + i, t)) ? INFINITY : -INFINITY;
+            }
+        bool touched = false;  // the partial rows hold this item's running minimum
+        for (int it = 0; it < iters; it++) {
+            const int gi = kl * iters + it;
+            const int st = gi % STAGES;
+            mbar_wait(&full[st], (uint32_t)((gi / STAGES) & 1));
+            unsigned needk = 0;
+            {
+                const float *a_f = Af + st * A_ST + (sg * RW) * TMW + lane;
+                const float *b_f = Bf + st * B_ST + (tg * RW) * TMBW + lane;
+#pragma unroll 1
+                for (int k = 0; k < KC; k++) {
+                    float a[RW], b[RW];
+                    const float *bk = b_f + k * TB * TMBW + soff[st * KC + k];
+#pragma unroll
+                    for (int i = 0; i < RW; i++) a[i] = a_f[k * TB * TMW + i * TMW];
+#pragma unroll
+                    for (int j = 0; j < RW; j++) b[j] = bk[j * TMBW];
+                    bool nk = false;
+#pragma unroll
+                    for (int i = 0; i < RW; i++)
+#pragma unroll
+                        for (int j = 0; j < RW; j++) nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
+                    needk |= (unsigned)nk << k;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (tid == PRODUCER && gi + STAGES < total) {
+                mbar_wait(&empty[st], (uint32_t)((gi / STAGES) & 1));
+                issue(gi + STAGES);
+            }
+            needk = __reduce_or_sync(0xffffffffu, needk);
+            if (needk) {  // exact fp64 splits, operands and running minimum in global memory
+                int i0, j0, m0, sp0;
+                coords(gi, i0, j0, m0, sp0);
+#pragma unroll
+                for (int i = 0; i < RW; i++) {
+                    double acc[RW];
+                    double *crow = p.C + cell_index(n, s_0 + i, min(t_0, n)) * p.pitch + mc;
+#pragma unroll
+                    for (int j = 0; j < RW; j++) acc[j] = (touched && t_0 + j <= n) ? crow[(int64_t)j * p.pitch] : INFINITY;
+#pragma unroll 1
+                    for (int k = 0; k < KC; k++) {
+                        if (!((needk >> k) & 1)) continue;
+                        const int sp = sp0 + k;
+                        const int mm = mc - wxp[sp - 1];
+                        const double a = __ldcg(p.A + a_index(s_0 + i, sp - 1) * p.pitch + mc);
+                        const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
+#pragma unroll
+                        for (int j = 0; j < RW; j++) {
+                            const double b = (mm >= 0 && t_0 + j <= n) ? bp[(int64_t)j * p.pitch] : INFINITY;
+                            acc[j] = dmin(acc[j], __dadd_rn(a, b));
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < RW; j++) {
+                        if (t_0 + j <= n && m <= p.S) crow[(int64_t)j * p.pitch] = acc[j];
+                        bestf[i][j] = bestf[i][j] == -INFINITY ? -INFINITY : __double2float_ru(acc[j]);
+                    }
+                }
+                touched = true;
+            }
+        }
+        if (!touched && m <= p.S) {  // no candidate below +inf: the partial is +inf
+#pragma unroll 1
+            for (int i = 0; i < RW; i++) {
+                double *crow = p.C + cell_index(n, s_0 + i, min(t_0, n)) * p.pitch + m;
+#pragma unroll
+                for (int j = 0; j < RW; j++)
+                    if (t_0 + j <= n) crow[(int64_t)j * p.pitch] = INFINITY;
+            }
+        }
+    }
+}
 
 #include "rotor_tiled_dep.cuh"
 
@@ -1066,9 +662,17 @@ bool make_map32(CUtensorMap *map, const float *base, int64_t rows, int64_t pitch
     cuuint64_t strides[1] = {(cuuint64_t)(pitch * 4)};
     cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
+    static int promo = -1;  // ROTOR_L2PROMO=0|64|128|256 (A/B runs)
+    if (promo < 0) {
+        const char *e = getenv("ROTOR_L2PROMO");
+        promo = e ? atoi(e) : 256;
+    }
+    const CUtensorMapL2promotion pr = promo == 0    ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+                                      : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+                                      : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
@@ -1088,15 +692,9 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     if (!attr) {
         if (cudaFuncSetAttribute(k_tile_middle<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tile_middle_pruned<8, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(SMEM_BYTES + 512 + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tile_middle_pruned<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(SMEM_BYTES + 512 + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tile_middle_pruned2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(SMEM_BYTES + 512 + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tile_middle_pruned3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(SMEM_BYTES + 512 + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
             cudaFuncSetAttribute(k_tile_middle_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(k_tile_middle_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
                 cudaSuccess)
             return -1;
         attr = true;
@@ -1107,10 +705,14 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
         !make_map(reinterpret_cast<CUtensorMap *>(ctx->tmC), p.C - kPad, rows + kPadRows, p.pitch, TMB, TB) ||
         !p.A32 || !p.C32 ||
         !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmA32), p.A32 - kPad, rows + kPadRows, p.pitch, TM, TB) ||
-        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmC32), p.C32 - kPad, rows + kPadRows, p.pitch, TMB32, TB))
+        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmC32), p.C32 - kPad, rows + kPadRows, p.pitch, TMB32, TB) ||
+        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmA32w), p.A32 - kPad, rows + kPadRows, p.pitch, TMW, TB) ||
+        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmC32w), p.C32 - kPad, rows + kPadRows, p.pitch, TMBW, TB))
         return -1;
     if (!p.flags || cudaMemsetAsync(p.flags, 0, leaf_flag_bytes(p.L, p.S), st) != cudaSuccess) return -1;
     ctx->phase_id = 0;
+    ctx->mid_ev = nullptr;
+    ctx->mid_cap = ctx->mid_n = 0;
     return 0;
 }
 
@@ -1132,39 +734,42 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
         const size_t smem = SMEM_BYTES + (p.n <= WX_SMEM_MAX ? (size_t)p.n * 4 : 0);
         const CUtensorMap &tmA = *reinterpret_cast<const CUtensorMap *>(ctx->tmA);
         const CUtensorMap &tmC = *reinterpret_cast<const CUtensorMap *>(ctx->tmC);
-        static int variant = -1;  // ROTOR_MIDDLE=exact|p82|p44|p2 (A/B runs)
+        static int variant = -1;  // ROTOR_MIDDLE=exact|f32|wide (A/B runs; default wide)
         if (variant < 0) {
             const char *e = getenv("ROTOR_MIDDLE");
-            variant = (e && !strcmp(e, "exact")) ? 0 : (e && !strcmp(e, "p82")) ? 1 : (e && !strcmp(e, "p44")) ? 2 : (e && !strcmp(e, "p2")) ? 3 : (e && !strcmp(e, "p3")) ? 4 : 5;
+            variant = (e && !strcmp(e, "exact")) ? 0 : (e && !strcmp(e, "f32")) ? 1 : 2;
         }
         const int nt = tile_hi - tile_lo;
-        const size_t psmem = smem + 512;
+        const bool timed = ctx->mid_ev && ctx->mid_n < ctx->mid_cap;
+        if (timed) cudaEventRecord(ctx->mid_ev[2 * ctx->mid_n], st);
         if (variant == 1)
-            k_tile_middle_pruned<8, 2><<<grid, THREADS, psmem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
-        else if (variant == 2)
-            k_tile_middle_pruned<4, 4><<<grid, THREADS, psmem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
-        else if (variant == 3)
-            k_tile_middle_pruned2<<<grid, THREADS, psmem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
-        else if (variant == 4)
-            k_tile_middle_pruned3<<<grid, THREADS, psmem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
-        else if (variant == 5)
             k_tile_middle_f32<<<grid, THREADS, F32Ring::bytes + (p.n <= F32_WX_MAX ? (size_t)p.n * 4 : 0), st>>>(
                 *reinterpret_cast<const CUtensorMap *>(ctx->tmA32), *reinterpret_cast<const CUtensorMap *>(ctx->tmC32),
                 p, delta, tile_lo, nt);
-        else
+        else if (variant == 2) {
+            const int items_w = nt * ((p.S + 1 + TMW - 1) / TMW);
+            k_tile_middle_wide<<<items_w < sms ? items_w : sms, THREADS,
+                                 WideRing::bytes + (p.n <= WIDE_WX_MAX ? (size_t)p.n * 4 : 0), st>>>(
+                *reinterpret_cast<const CUtensorMap *>(ctx->tmA32w),
+                *reinterpret_cast<const CUtensorMap *>(ctx->tmC32w), p, delta, tile_lo, nt);
+        } else
             k_tile_middle<KC, STAGES><<<grid, THREADS, smem, st>>>(tmA, tmC, p, delta, tile_lo, tile_hi - tile_lo);
+        if (timed) cudaEventRecord(ctx->mid_ev[2 * ctx->mid_n++ + 1], st);
         launches++;
     }
     return launches + launch_dependent(p, delta, tile_lo, tile_hi, st, p.flags, ctx->phase_id);
 }
 
 // Returns the number of kernels launched, or -1 on a launch/setup error.
-int launch_fill_tiled(const Problem &p, cudaStream_t st) {
+int launch_fill_tiled(const Problem &p, cudaStream_t st, cudaEvent_t *mid_ev, int mid_cap, int *mid_n) {
     TiledCtx ctx;
     if (tiled_prepare(p, &ctx, st)) return -1;
+    ctx.mid_ev = mid_ev;
+    ctx.mid_cap = mid_cap;
     const int nb = tiled_nb(p.n);
     int launches = 0;
     for (int delta = 0; delta < nb; delta++) launches += tiled_delta(p, &ctx, delta, 0, nb - delta, st);
+    if (mid_n) *mid_n = ctx.mid_n;
     return launches;
 }
 

@@ -31,7 +31,9 @@ size_t batch_slot_bytes(int L_max, int S);
 void launch_batch(const BatchArgs &b, int n_slots, cudaStream_t st);
 
 // Tiled fill (rotor_fill_tiled.cu). Returns the number of kernels launched (-1: setup error).
-int launch_fill_tiled(const Problem &p, cudaStream_t st);
+// mid_ev (optional, 2 * mid_cap events): recorded around each middle-kernel launch
+int launch_fill_tiled(const Problem &p, cudaStream_t st, cudaEvent_t *mid_ev = nullptr, int mid_cap = 0,
+                      int *mid_n = nullptr);
 size_t tiled_extra_bytes(int L, int S);
 
 // Pieces of the tiled fill for a sharded (multi-rank) solve.
@@ -40,7 +42,11 @@ struct TiledCtx {
     alignas(64) unsigned char tmC[128];  // CUtensorMap of the C table
     alignas(64) unsigned char tmA32[128];  // fp32 shadow of A
     alignas(64) unsigned char tmC32[128];  // fp32 shadow of C
+    alignas(64) unsigned char tmA32w[128];  // the same with the wide middle kernel's boxes
+    alignas(64) unsigned char tmC32w[128];
     int phase_id;                        // leaf launches so far (look-back flag epochs)
+    cudaEvent_t *mid_ev;                 // optional (profiling): event pairs around the middle launches
+    int mid_cap, mid_n;                  // pairs available / recorded
 };
 int tiled_nb(int n);  // number of TB-stage blocks
 int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st);

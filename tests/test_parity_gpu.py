@@ -156,10 +156,11 @@ def test_tiled_block_boundaries(R, oracle_mod, L):
     check_against_oracle(R, O, ch2, 24, 24, kernel="tiled")
 
 
-@pytest.mark.parametrize("S", [15, 16, 17, 127, 128, 129, 255, 257, 520])
+@pytest.mark.parametrize("S", [15, 16, 17, 31, 32, 33, 63, 64, 127, 128, 129, 255, 257, 520])
 def test_tiled_m_chunk_boundaries(R, oracle_mod, S):
-    """S + 1 around the m-chunks of the tiled kernels (16 m per middle item and
-    sub-product warp, 128 m per leaf CTA, 32 / 128 look-back chunks), with
+    """S + 1 around the m-chunks of the tiled kernels (32 m per wide middle item,
+    16 m per exact/f32 middle item and sub-product warp, 128 m per leaf CTA,
+    32 / 128 look-back chunks), with
     shifts from a fraction of a chunk to several chunks (big sizes, tight and
     loose limits): full tables bit-exact, both modes."""
     O = oracle_mod
@@ -169,6 +170,43 @@ def test_tiled_m_chunk_boundaries(R, oracle_mod, S):
         M = max(1, int(sum(int(x) for x in ch.wbx) * f))
         check_against_oracle(R, O, ch, M, S, kernel="tiled")
     check_against_oracle(R, O, ch, M, S, kernel="tiled", restricted=True)
+
+
+_VARIANT_SCRIPT = r"""
+import sys
+import numpy as np
+import __graft_entry__ as ge
+ge.build_library()
+import chaingen as G, oracle as O, paper_1911_13214_b200 as R
+cases = [(G.config2().chain, G.config2().mem_limit, G.config2().slots)]
+for L, S in ((95, 33), (64, 129)):
+    ch = G.random_chain(G.SplitMix64(7000 + L), L, real_times=True, big=True)
+    cases.append((ch, max(1, int(sum(int(x) for x in ch.wbx) * 0.22)), S))
+for ch, M, S in cases:
+    res = R.solve(ch, M, S, kernel="tiled")
+    C, _ = R.export_tables(ch.L + 1, S, D=False)
+    o = O.OracleSolve(ch, M, S)
+    Co, _ = o.tables()
+    assert np.array_equal(C.view(np.uint64), Co.view(np.uint64)), (ch.name, ch.L, S)
+    assert res.op_list() == (o.reconstruct() or [])
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("variant", ["exact", "f32"])
+def test_middle_kernel_variants(R, variant):
+    """The non-default middle kernels (ROTOR_MIDDLE, read once per process: the
+    unpruned fp64 k_tile_middle and the 16-m fp32-filter variant) stay
+    bit-exact against the oracle — run in a subprocess with the variable set."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ROTOR_MIDDLE=variant, PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
 
 
 def test_device_resident_path(R, oracle_mod):
