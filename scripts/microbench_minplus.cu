@@ -4,6 +4,9 @@
 //   0: v < acc ? v : acc on doubles       (DADD + DSETP + 2 FSEL)
 //   1: 64-bit integer min on the bit patterns of non-negative doubles
 //   2: DADD only (upper bound of the fp64 pipe)
+//   5: the pruned middle kernel's filter on fp32 operands in shared memory
+//      (FADD.RM + FSETP.LT.OR per candidate, 8 x 8 register tile, one m per
+//      lane, per-split fire mask OR-reduced over the warp) — its issue ceiling
 //   4: fp32 lower-bound filter (cvt.rm.f32.f64 of the operands, FADD.RM, FMNMX;
 //      per 8 splits one exact compare of the chunk minimum against the fp64
 //      accumulator) — the pruned middle kernel's steady state with no exact pass
@@ -83,6 +86,68 @@ __global__ void __launch_bounds__(256) kern(double *out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// MODE 5 kernel: operands fp32 [8 splits][8 rows][32 m] in shared memory
+__global__ void __launch_bounds__(512, 1) kern_filter(float *out, int iters) {
+    __shared__ float As[8][8][32];
+    __shared__ float Bs[8][8][32];
+    const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < 8 * 8 * 32; i += blockDim.x) {
+        (&As[0][0][0])[i] = 1.0f + (i % 7) * 0.125f;
+        (&Bs[0][0][0])[i] = 2.0f + (i % 5) * 0.25f;
+    }
+    __syncthreads();
+    float bestf[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; i++)
+#pragma unroll
+        for (int j = 0; j < 8; j++) bestf[i][j] = 0.5f + 0.01f * (i * 8 + j) + 0.001f * lane;
+    unsigned acc = 0;
+    for (int it = 0; it < iters; it++) {
+        unsigned needk = 0;
+#pragma unroll 1
+        for (int k = 0; k < 8; k++) {
+            const int kk = (k + it) & 7;
+            float a[8], b[8];
+#pragma unroll
+            for (int i = 0; i < 8; i++) a[i] = As[kk][i][lane];
+#pragma unroll
+            for (int j = 0; j < 8; j++) b[j] = Bs[kk][j][lane];
+            bool nk = false;
+#pragma unroll
+            for (int i = 0; i < 8; i++)
+#pragma unroll
+                for (int j = 0; j < 8; j++) nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
+            needk |= (unsigned)nk << k;
+        }
+        acc += __reduce_or_sync(0xffffffffu, needk);
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = (float)acc;
+}
+
+void run_filter() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int blocks = sms, threads = 512, iters = 2000;
+    float *out;
+    cudaMalloc(&out, blocks * threads * sizeof(float));
+    kern_filter<<<blocks, threads>>>(out, 4);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    kern_filter<<<blocks, threads>>>(out, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double tr = (double)blocks * threads * iters * 8 * 64;
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("%-28s 8x8 tile  %.3e candidates/s  (%.1f cand/clk/SM at %d MHz)  err=%s\n", "middle filter (fp32 smem)",
+           tr / (ms * 1e-3), tr / (ms * 1e-3) / sms / (clk * 1e3), clk / 1000, cudaGetErrorString(cudaGetLastError()));
+    cudaFree(out);
+}
+
 template <int MODE, int RS, int RT>
 void run(const char *name) {
     int sms = 0;
@@ -109,6 +174,7 @@ void run(const char *name) {
 }
 
 int main() {
+    run_filter();
     run<0, 4, 4>("dsetp-min");
     run<0, 4, 8>("dsetp-min");
     run<0, 8, 8>("dsetp-min");
