@@ -19,6 +19,22 @@ def test_transitions_formula():
     assert bench.n_transitions(L, S) == brute
 
 
+def test_middle_transitions_bruteforce():
+    """The middle kernel's candidates: every split s' of a cell (s,t) that lies in a
+    32-stage block strictly between the blocks of s and t (enumerated cell by cell),
+    at every m; a subset of the nominal transitions."""
+    TB = 32
+    for L, S in ((70, 3), (96, 5), (130, 2)):
+        n = L + 1
+        brute = 0
+        for s in range(1, n + 1):
+            for t in range(s + 1, n + 1):
+                bs, bt = (s - 1) // TB, (t - 1) // TB
+                brute += sum(1 for sp in range(s + 1, t + 1) if bs < (sp - 1) // TB < bt)
+        assert bench.middle_transitions(L, S, TB) == brute * (S + 1)
+        assert bench.middle_transitions(L, S, TB) < bench.n_transitions(L, S)
+
+
 def test_alg_bytes_wavefront_bruteforce():
     """Distinct rows read per diagonal, by enumerating the cells each candidate touches."""
     L, S = 9, 3
