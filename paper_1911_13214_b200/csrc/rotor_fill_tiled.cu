@@ -550,7 +550,18 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int t = t_0 + j;
                 bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + i, t)) ? INFINITY : -INFINITY;
             }
-        bool touched = false;  // the partial rows hold this item's running minimum
+        // the partial rows start at +inf; the rare exact passes fold their
+        // candidates in with 64-bit atomic min (RED, nothing read back: every
+        // value is >= 0 or +inf, so the fp64 order is the uint64 order, Q13)
+        if (m <= p.S) {
+#pragma unroll 1
+            for (int i = 0; i < RW; i++) {
+                double *crow = p.C + cell_index(n, s_0 + i, min(t_0, n)) * p.pitch + m;
+#pragma unroll
+                for (int j = 0; j < RW; j++)
+                    if (t_0 + j <= n) crow[(int64_t)j * p.pitch] = INFINITY;
+            }
+        }
         for (int it = 0; it < iters; it++) {
             const int gi = kl * iters + it;
             const int st = gi % STAGES;
@@ -582,44 +593,36 @@ __global__ void __launch_bounds__(THREADS, 1)
                 issue(gi + STAGES);
             }
             needk = __reduce_or_sync(0xffffffffu, needk);
-            if (needk) {  // exact fp64 splits, operands and running minimum in global memory
+            if (needk) {  // exact fp64 splits: operands from global memory, one round trip per split
                 int i0, j0, m0, sp0;
                 coords(gi, i0, j0, m0, sp0);
-#pragma unroll
-                for (int i = 0; i < RW; i++) {
-                    double acc[RW];
-                    double *crow = p.C + cell_index(n, s_0 + i, min(t_0, n)) * p.pitch + mc;
-#pragma unroll
-                    for (int j = 0; j < RW; j++) acc[j] = (touched && t_0 + j <= n) ? crow[(int64_t)j * p.pitch] : INFINITY;
 #pragma unroll 1
-                    for (int k = 0; k < KC; k++) {
-                        if (!((needk >> k) & 1)) continue;
-                        const int sp = sp0 + k;
-                        const int mm = mc - wxp[sp - 1];
-                        const double a = __ldcg(p.A + a_index(s_0 + i, sp - 1) * p.pitch + mc);
-                        const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
+                for (int k = 0; k < KC; k++) {
+                    if (!((needk >> k) & 1)) continue;
+                    const int sp = sp0 + k;
+                    const int mm = mc - wxp[sp - 1];
+                    const double *ap = p.A + a_index(s_0, sp - 1) * p.pitch + mc;
+                    const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
+                    double ad[RW], bd[RW];
+#pragma unroll
+                    for (int i = 0; i < RW; i++) ad[i] = __ldcg(ap + (int64_t)i * p.pitch);
+#pragma unroll
+                    for (int j = 0; j < RW; j++)
+                        bd[j] = (mm >= 0 && t_0 + j <= n) ? __ldcg(bp + (int64_t)j * p.pitch) : INFINITY;
+#pragma unroll
+                    for (int i = 0; i < RW; i++) {
+                        unsigned long long *crow = reinterpret_cast<unsigned long long *>(
+                            p.C + cell_index(n, s_0 + i, min(t_0, n)) * p.pitch + mc);
 #pragma unroll
                         for (int j = 0; j < RW; j++) {
-                            const double b = (mm >= 0 && t_0 + j <= n) ? bp[(int64_t)j * p.pitch] : INFINITY;
-                            acc[j] = dmin(acc[j], __dadd_rn(a, b));
+                            const double v = __dadd_rn(ad[i], bd[j]);
+                            if (t_0 + j <= n && m <= p.S && v < INFINITY)
+                                atomicMin(crow + (int64_t)j * p.pitch, (unsigned long long)__double_as_longlong(v));
+                            // bestf stays >= the running minimum: min(old bound, ru(v))
+                            bestf[i][j] = fminf(bestf[i][j], __double2float_ru(v));
                         }
                     }
-#pragma unroll
-                    for (int j = 0; j < RW; j++) {
-                        if (t_0 + j <= n && m <= p.S) crow[(int64_t)j * p.pitch] = acc[j];
-                        bestf[i][j] = bestf[i][j] == -INFINITY ? -INFINITY : __double2float_ru(acc[j]);
-                    }
                 }
-                touched = true;
-            }
-        }
-        if (!touched && m <= p.S) {  // no candidate below +inf: the partial is +inf
-#pragma unroll 1
-            for (int i = 0; i < RW; i++) {
-                double *crow = p.C + cell_index(n, s_0 + i, min(t_0, n)) * p.pitch + m;
-#pragma unroll
-                for (int j = 0; j < RW; j++)
-                    if (t_0 + j <= n) crow[(int64_t)j * p.pitch] = INFINITY;
             }
         }
     }
