@@ -41,3 +41,7 @@ fi
 if has san; then
   bash scripts/sanitize.sh "$TAG/san" 2>&1 | tail -4
 fi
+if has sharded; then
+  ROTOR_FORCE_SHARDED=1 timeout 600 python bench.py --no-cpu-baseline > "$OUT/bench_sharded_1rank.json" 2> "$OUT/bench_sharded_1rank.err"
+  echo "bench sharded (1 rank) rc=$?"; cut -c1-200 "$OUT/bench_sharded_1rank.json"
+fi
