@@ -474,7 +474,7 @@ static_assert((TB / RW) * (TB / RW) * TMW == THREADS, "one lane per (m, 8x8 tile
 
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle_wide(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmC32,
-                       Problem p, int delta, int tile_lo, int n_tiles) {
+                       Problem p, int delta, int tile_lo, int n_tiles, int coarse) {
     using R = WideRing;
     constexpr int KC = R::KC, STAGES = R::STAGES, A_ST = R::A_ST, B_ST = R::B_ST;
     extern __shared__ __align__(1024) float fsm[];
@@ -550,6 +550,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int t = t_0 + j;
                 bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + i, t)) ? INFINITY : -INFINITY;
             }
+        float maxb = -INFINITY;  // >= every bestf of the lane
+#pragma unroll
+        for (int i = 0; i < RW; i++)
+#pragma unroll
+            for (int j = 0; j < RW; j++) maxb = fmaxf(maxb, bestf[i][j]);
         // the partial rows start at +inf; the rare exact passes fold their
         // candidates in with 64-bit atomic min (RED, nothing read back: every
         // value is >= 0 or +inf, so the fp64 order is the uint64 order, Q13)
@@ -578,12 +583,28 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int i = 0; i < RW; i++) a[i] = a_f[k * TB * TMW + i * TMW];
 #pragma unroll
                     for (int j = 0; j < RW; j++) b[j] = bk[j * TMBW];
-                    bool nk = false;
+                    // coarse bound first: fadd_rd(min a, min b) <= every lb of the
+                    // split (monotone rounding) and maxb >= every bestf, so when it
+                    // is >= maxb on every lane no candidate can fire and the 64
+                    // per-cell compares are skipped
+                    bool maybe = true;
+                    if (coarse) {
+                        float ma = a[0], mb = b[0];
 #pragma unroll
-                    for (int i = 0; i < RW; i++)
+                        for (int i = 1; i < RW; i++) {
+                            ma = fminf(ma, a[i]);
+                            mb = fminf(mb, b[i]);
+                        }
+                        maybe = __fadd_rd(ma, mb) < maxb;
+                    }
+                    if (__any_sync(0xffffffffu, maybe)) {
+                        bool nk = false;
 #pragma unroll
-                        for (int j = 0; j < RW; j++) nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
-                    needk |= (unsigned)nk << k;
+                        for (int i = 0; i < RW; i++)
+#pragma unroll
+                            for (int j = 0; j < RW; j++) nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
+                        needk |= (unsigned)nk << k;
+                    }
                 }
             }
             __syncwarp();
@@ -623,6 +644,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                     }
                 }
+                maxb = -INFINITY;
+#pragma unroll
+                for (int i = 0; i < RW; i++)
+#pragma unroll
+                    for (int j = 0; j < RW; j++) maxb = fmaxf(maxb, bestf[i][j]);
             }
         }
     }
@@ -737,6 +763,11 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
         const size_t smem = SMEM_BYTES + (p.n <= WX_SMEM_MAX ? (size_t)p.n * 4 : 0);
         const CUtensorMap &tmA = *reinterpret_cast<const CUtensorMap *>(ctx->tmA);
         const CUtensorMap &tmC = *reinterpret_cast<const CUtensorMap *>(ctx->tmC);
+        static int coarse = -1;  // ROTOR_COARSE=0|1 (A/B)
+        if (coarse < 0) {
+            const char *e = getenv("ROTOR_COARSE");
+            coarse = e ? atoi(e) : 1;
+        }
         static int variant = -1;  // ROTOR_MIDDLE=exact|f32|wide (A/B runs; default wide)
         if (variant < 0) {
             const char *e = getenv("ROTOR_MIDDLE");
@@ -754,7 +785,7 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
             k_tile_middle_wide<<<items_w < sms ? items_w : sms, THREADS,
                                  WideRing::bytes + (p.n <= WIDE_WX_MAX ? (size_t)p.n * 4 : 0), st>>>(
                 *reinterpret_cast<const CUtensorMap *>(ctx->tmA32w),
-                *reinterpret_cast<const CUtensorMap *>(ctx->tmC32w), p, delta, tile_lo, nt);
+                *reinterpret_cast<const CUtensorMap *>(ctx->tmC32w), p, delta, tile_lo, nt, coarse);
         } else
             k_tile_middle<KC, STAGES><<<grid, THREADS, smem, st>>>(tmA, tmC, p, delta, tile_lo, tile_hi - tile_lo);
         if (timed) cudaEventRecord(ctx->mid_ev[2 * ctx->mid_n++ + 1], st);
