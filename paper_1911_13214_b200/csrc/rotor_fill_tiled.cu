@@ -550,11 +550,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int t = t_0 + j;
                 bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + i, t)) ? INFINITY : -INFINITY;
             }
-        float maxb = -INFINITY;  // >= every bestf of the lane
+        float maxq[2][2];  // >= every bestf of the lane's 4 x 4 quadrants
 #pragma unroll
-        for (int i = 0; i < RW; i++)
+        for (int qa = 0; qa < 2; qa++)
 #pragma unroll
-            for (int j = 0; j < RW; j++) maxb = fmaxf(maxb, bestf[i][j]);
+            for (int qb = 0; qb < 2; qb++) {
+                maxq[qa][qb] = -INFINITY;
+#pragma unroll
+                for (int i = 4 * qa; i < 4 * qa + 4; i++)
+#pragma unroll
+                    for (int j = 4 * qb; j < 4 * qb + 4; j++) maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
+            }
         // the partial rows start at +inf; the rare exact passes fold their
         // candidates in with 64-bit atomic min (RED, nothing read back: every
         // value is >= 0 or +inf, so the fp64 order is the uint64 order, Q13)
@@ -583,28 +589,35 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int i = 0; i < RW; i++) a[i] = a_f[k * TB * TMW + i * TMW];
 #pragma unroll
                     for (int j = 0; j < RW; j++) b[j] = bk[j * TMBW];
-                    // coarse bound first: fadd_rd(min a, min b) <= every lb of the
-                    // split (monotone rounding) and maxb >= every bestf, so when it
-                    // is >= maxb on every lane no candidate can fire and the 64
-                    // per-cell compares are skipped
-                    bool maybe = true;
-                    if (coarse) {
-                        float ma = a[0], mb = b[0];
+                    // coarse bounds first: per 4 x 4 quadrant (qa, qb) of the lane's
+                    // tile, fadd_rd(min a over its rows, min b over its columns) is
+                    // <= every lb of the quadrant (monotone rounding) and maxq >= every
+                    // bestf of it; a quadrant is compared cell by cell only if that
+                    // bound is below maxq on some lane of the warp
+                    float ma[2], mb[2];
 #pragma unroll
-                        for (int i = 1; i < RW; i++) {
-                            ma = fminf(ma, a[i]);
-                            mb = fminf(mb, b[i]);
-                        }
-                        maybe = __fadd_rd(ma, mb) < maxb;
+                    for (int h = 0; h < 2; h++) {
+                        ma[h] = fminf(fminf(a[4 * h], a[4 * h + 1]), fminf(a[4 * h + 2], a[4 * h + 3]));
+                        mb[h] = fminf(fminf(b[4 * h], b[4 * h + 1]), fminf(b[4 * h + 2], b[4 * h + 3]));
                     }
-                    if (__any_sync(0xffffffffu, maybe)) {
-                        bool nk = false;
+                    bool nk = false;
+                    const float mall = fmaxf(fmaxf(maxq[0][0], maxq[0][1]), fmaxf(maxq[1][0], maxq[1][1]));
+                    if (__any_sync(0xffffffffu, !coarse || __fadd_rd(fminf(ma[0], ma[1]), fminf(mb[0], mb[1])) < mall)) {
 #pragma unroll
-                        for (int i = 0; i < RW; i++)
+                        for (int qa = 0; qa < 2; qa++)
 #pragma unroll
-                            for (int j = 0; j < RW; j++) nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
-                        needk |= (unsigned)nk << k;
+                            for (int qb = 0; qb < 2; qb++) {
+                                const bool maybe = !coarse || __fadd_rd(ma[qa], mb[qb]) < maxq[qa][qb];
+                                if (__any_sync(0xffffffffu, maybe)) {
+#pragma unroll
+                                    for (int i = 4 * qa; i < 4 * qa + 4; i++)
+#pragma unroll
+                                        for (int j = 4 * qb; j < 4 * qb + 4; j++)
+                                            nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
+                                }
+                            }
                     }
+                    needk |= (unsigned)nk << k;
                 }
             }
             __syncwarp();
@@ -644,11 +657,17 @@ __global__ void __launch_bounds__(THREADS, 1)
                         }
                     }
                 }
-                maxb = -INFINITY;
 #pragma unroll
-                for (int i = 0; i < RW; i++)
+                for (int qa = 0; qa < 2; qa++)
 #pragma unroll
-                    for (int j = 0; j < RW; j++) maxb = fmaxf(maxb, bestf[i][j]);
+                    for (int qb = 0; qb < 2; qb++) {
+                        maxq[qa][qb] = -INFINITY;
+#pragma unroll
+                        for (int i = 4 * qa; i < 4 * qa + 4; i++)
+#pragma unroll
+                            for (int j = 4 * qb; j < 4 * qb + 4; j++)
+                                maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
+                    }
             }
         }
     }
