@@ -162,6 +162,24 @@ def middle_transitions(L: int, S: int, TB: int = 32) -> int:
     return tot * (S + 1)
 
 
+def middle_alg_bytes(L: int, S: int, TB: int = 32) -> int:
+    """Bytes the middle kernel must move per solve (DESIGN 5.2): for every tile
+    (I, J), J - I >= 2, split s' of its middle range and m, the fp32 shadow
+    operands A32(s, s'-1, m) of its real rows s and C32(s', t, m - w) of its
+    real columns t are read once (4 B each), and every real cell's partial
+    minimum is written once (8 B) — the operand reuse a tile allows, nothing
+    re-read."""
+    n = L + 1
+    nb = (n + TB - 1) // TB
+    tot = 0
+    for I in range(nb):
+        cs = min(n, TB * (I + 1)) - TB * I
+        for J in range(I + 2, nb):
+            ct = min(n, TB * (J + 1)) - TB * J
+            tot += 4 * (cs + ct) * (J - I - 1) * TB + 8 * cs * ct
+    return tot * (S + 1)
+
+
 def ncu_kernel_step_traffic(key: str, kernel: str):
     """DRAM bytes of one kernel's launches in one solve (committed ncu launch-list summary)."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -550,30 +568,39 @@ def run_ours(args):
     peaks, peak_kind = measured_peaks()
     fill_avg_ms = sum(fill_ms) / len(fill_ms)
     if kernel in ("auto", "tiled"):
-        # Dominant kernel: the pruned middle (DESIGN 5.2).  Every candidate costs one
-        # FADD.RM (FMA pipe) + one FSETP.LT.OR on the ALU pipe (16 lanes/clk per SM
-        # sub-partition, 64 per SM); the rare exact fp64 recomputes run on the fp64
-        # pipe.  Peak = 148 SMs x 64 candidates/clk x sm_max_mhz.
+        # Dominant kernel: the pruned middle (DESIGN 5.2).  With the coarse bounds it
+        # compares only a fraction of the candidates cell by cell, and what it
+        # cannot avoid is streaming the fp32 shadow operands of every (tile, split,
+        # m) once: it is bound by HBM (26% of warp samples wait for TMA data at
+        # Delta = 16, profiles/r01_tiled_v10.md).  achieved = middle_alg_bytes per
+        # solve / the middle launches' CUDA-event time; peak = measured HBM.
         clk_mhz = float(peaks.get("sm_max_mhz", 1965.0))
         mid_avg_ms = sum(mid_ms) / len(mid_ms)
         tm = middle_transitions(L, S)
-        peak = 148 * 64.0 * clk_mhz * 1e6 / 1e9  # Gtransitions/s
-        achieved = tm / (mid_avg_ms / 1e3) / 1e9
+        mb_alg = middle_alg_bytes(L, S)
+        peak = float(peaks["hbm_gbs"])
+        achieved = mb_alg / (mid_avg_ms / 1e3) / 1e9  # GB/s
+        alu_peak = 148 * 64.0 * clk_mhz * 1e6 / 1e9  # Gcandidates/s, one FSETP per candidate
+        alu_ach = tm / (mid_avg_ms / 1e3) / 1e9
         # the whole fill against the exact fp64 evaluation model (DADD 64 lanes/clk +
         # DSETP 32 lanes/clk per SM on the fp64 pipe -> 21.33 transitions/clk/SM)
         fill_peak = 148 * (64.0 / 3.0) * clk_mhz * 1e6 / 1e9
         fill_ach = tr / (fill_avg_ms / 1e3) / 1e9
-        roofline = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gtransitions/s",
-                    "frac": achieved / peak,
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "peak_source": peak_kind,
                     "traffic": ncu_kernel_step_traffic("tiled_solve", "k_tile_middle_wide"),
                     "traffic_scope": "DRAM read+write bytes of all middle launches of one solve (ncu launch list, "
                                      "profiles/ncu_summary.json tiled_solve)",
-                    "kernel": "k_tile_middle_wide (pruned middle: fp32 lower-bound filter, exact fp64 recompute)",
-                    "peak_model": "148 SMs x sm_max_mhz x 64 candidates/clk/SM (one FSETP per candidate on the "
-                                  "ALU pipe)",
+                    "alg_bytes_per_step": mb_alg,
+                    "kernel": "k_tile_middle_wide (pruned middle: fp32 shadow boxes, coarse + per-cell lower-bound "
+                              "filter, exact fp64 recompute with atomic min)",
                     "transitions_per_step": tm, "middle_ms_per_step": mid_avg_ms,
                     "middle_launches_per_step": mid_launches,
                     "middle_share_of_fill": mid_avg_ms / fill_avg_ms,
+                    "alu_model": {"achieved": alu_ach, "peak": alu_peak, "frac": alu_ach / alu_peak,
+                                  "unit": "Gtransitions/s",
+                                  "peak_model": "148 SMs x sm_max_mhz x 64 candidates/clk/SM (one FSETP per "
+                                                "candidate on the ALU pipe; the coarse bounds skip most of them)"},
                     "fill": {"achieved": fill_ach, "peak": fill_peak, "frac": fill_ach / fill_peak,
                              "unit": "Gtransitions/s", "ms_per_step": fill_avg_ms, "launches_per_step": fill_launches,
                              "peak_model": "148 SMs x sm_max_mhz x 21.33 transitions/clk/SM (exact fp64 evaluation: "

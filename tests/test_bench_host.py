@@ -35,6 +35,23 @@ def test_middle_transitions_bruteforce():
         assert bench.middle_transitions(L, S, TB) < bench.n_transitions(L, S)
 
 
+def test_middle_alg_bytes_bruteforce():
+    """fp32 operand reads (one per real row / column, split and m) plus one 8-byte
+    partial write per real cell and m, enumerated tile by tile."""
+    TB = 32
+    for L, S in ((70, 3), (130, 2)):
+        n = L + 1
+        nb = (n + TB - 1) // TB
+        brute = 0
+        for I in range(nb):
+            rows = [s for s in range(TB * I + 1, TB * I + TB + 1) if s <= n]
+            for J in range(I + 2, nb):
+                cols = [t for t in range(TB * J + 1, TB * J + TB + 1) if t <= n]
+                splits = range(TB * (I + 1) + 1, TB * J + 1)
+                brute += sum(4 * len(rows) + 4 * len(cols) for _ in splits) + 8 * len(rows) * len(cols)
+        assert bench.middle_alg_bytes(L, S, TB) == brute * (S + 1)
+
+
 def test_alg_bytes_wavefront_bruteforce():
     """Distinct rows read per diagonal, by enumerating the cells each candidate touches."""
     L, S = 9, 3
