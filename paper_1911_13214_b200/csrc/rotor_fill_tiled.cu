@@ -464,18 +464,21 @@ __global__ void __launch_bounds__(THREADS, 1)
 // fired (per-split mask OR-reduced over the warp).
 // ---------------------------------------------------------------------------
 constexpr int TMW = 32, TMBW = TMW + 4, RW = 8;
+template <int KC_, int STAGES_>
 struct WideRing {
-    static constexpr int KC = 4, STAGES = 6;
+    static constexpr int KC = KC_, STAGES = STAGES_;
     static constexpr int A_ST = KC * TB * TMW, B_ST = KC * TB * TMBW;  // floats per stage
     static constexpr size_t bytes = (size_t)STAGES * (A_ST + B_ST) * 4 + 2 * STAGES * 8 + STAGES * KC * 4 + 64;
 };
-constexpr int WIDE_WX_MAX = (int)((227 * 1024 - WideRing::bytes) / 4);
+constexpr int WKC = 4, WSTAGES = 4;  // ring of the wide middle (see tiled_delta)
+constexpr int WIDE_WX_MAX = (int)((227 * 1024 - WideRing<WKC, WSTAGES>::bytes) / 4);
 static_assert((TB / RW) * (TB / RW) * TMW == THREADS, "one lane per (m, 8x8 tile)");
 
+template <int KCW, int STG>
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle_wide(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmC32,
                        Problem p, int delta, int tile_lo, int n_tiles, int coarse) {
-    using R = WideRing;
+    using R = WideRing<KCW, STG>;
     constexpr int KC = R::KC, STAGES = R::STAGES, A_ST = R::A_ST, B_ST = R::B_ST;
     extern __shared__ __align__(1024) float fsm[];
     float *Af = fsm;                 // [STAGES][KC][TB s][TMW]
@@ -742,8 +745,8 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
                                  (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
             cudaFuncSetAttribute(k_tile_middle_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
                 cudaSuccess ||
-            cudaFuncSetAttribute(k_tile_middle_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-                cudaSuccess)
+            cudaFuncSetAttribute(k_tile_middle_wide<WKC, WSTAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 227 * 1024) != cudaSuccess)
             return -1;
         attr = true;
     }
@@ -801,10 +804,16 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
                 p, delta, tile_lo, nt);
         else if (variant == 2) {
             const int items_w = nt * ((p.S + 1 + TMW - 1) / TMW);
-            k_tile_middle_wide<<<items_w < sms ? items_w : sms, THREADS,
-                                 WideRing::bytes + (p.n <= WIDE_WX_MAX ? (size_t)p.n * 4 : 0), st>>>(
-                *reinterpret_cast<const CUtensorMap *>(ctx->tmA32w),
-                *reinterpret_cast<const CUtensorMap *>(ctx->tmC32w), p, delta, tile_lo, nt, coarse);
+            // ring geometry (same-box A/B, ms of middle per config-4 solve): KC = 4 x
+            // 6 stages 79.1, x 5 77.3, x 4 76.8, x 3 76.6; KC = 8 x 3 83.5 — the
+            // shallower ring leaves more of the SM's shared-memory/L1 carve-out
+            // to L1 (spill reloads, exact-pass operands)
+            const size_t wx_b = p.n <= WIDE_WX_MAX ? (size_t)p.n * 4 : 0;
+            const CUtensorMap &ma = *reinterpret_cast<const CUtensorMap *>(ctx->tmA32w);
+            const CUtensorMap &mc = *reinterpret_cast<const CUtensorMap *>(ctx->tmC32w);
+            const int gw = items_w < sms ? items_w : sms;
+            k_tile_middle_wide<WKC, WSTAGES><<<gw, THREADS, WideRing<WKC, WSTAGES>::bytes + wx_b, st>>>(
+                ma, mc, p, delta, tile_lo, nt, coarse);
         } else
             k_tile_middle<KC, STAGES><<<grid, THREADS, smem, st>>>(tmA, tmC, p, delta, tile_lo, tile_hi - tile_lo);
         if (timed) cudaEventRecord(ctx->mid_ev[2 * ctx->mid_n++ + 1], st);
