@@ -193,17 +193,19 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("variant", ["exact", "f32"])
+@pytest.mark.parametrize("variant", ["exact", "f32", "nocoarse"])
 def test_middle_kernel_variants(R, variant):
-    """The non-default middle kernels (ROTOR_MIDDLE, read once per process: the
-    unpruned fp64 k_tile_middle and the 16-m fp32-filter variant) stay
-    bit-exact against the oracle — run in a subprocess with the variable set."""
+    """The non-default middle kernels (read once per process: ROTOR_MIDDLE=exact,
+    the unpruned fp64 k_tile_middle; =f32, the 16-m fp32-filter variant;
+    ROTOR_COARSE=0, the default kernel without its coarse bounds) stay bit-exact
+    against the oracle — run in a subprocess with the variable set."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, ROTOR_MIDDLE=variant, PYTHONPATH=root)
+    knob = {"nocoarse": {"ROTOR_COARSE": "0"}}.get(variant, {"ROTOR_MIDDLE": variant})
+    env = dict(os.environ, PYTHONPATH=root, **knob)
     r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
