@@ -58,6 +58,25 @@ def parse():
     return ap.parse_args()
 
 
+def init_nccl(dist, dev):
+    """init_process_group("nccl") with the process's stdout silenced at the fd level
+    while the communicator comes up (NCCL writes its version banner there), so
+    rank 0's stdout carries only the JSON line."""
+    sys.stdout.flush()
+    saved, null = os.dup(1), os.open(os.devnull, os.O_WRONLY)
+    os.dup2(null, 1)
+    try:
+        dist.init_process_group("nccl", device_id=dev)
+        dist.barrier()
+        import torch
+
+        torch.cuda.synchronize()
+    finally:
+        os.dup2(saved, 1)
+        os.close(saved)
+        os.close(null)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -278,7 +297,7 @@ def run_batched(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        init_nccl(dist, dev)
         pg = dist
     import __graft_entry__ as ge
 
@@ -382,7 +401,7 @@ def run_sharded(args):
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    init_nccl(dist, dev)
     import __graft_entry__ as ge
 
     if rank == 0:
@@ -488,7 +507,7 @@ def run_ours(args):
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        init_nccl(dist, dev)
         pg = dist
     import __graft_entry__ as ge
 
