@@ -428,9 +428,11 @@ def run_sharded(args):
     clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    launches = 0
     for _ in range(args.steps):
         eng.restart()
         res = solve_sharded(eng)  # finish() synchronises (reads the cost back)
+        launches += eng.shard.launches()
     e1.record(stream)
     torch.cuda.synchronize()
     dist.barrier()
@@ -483,6 +485,7 @@ def run_sharded(args):
                          "kernel": "whole sharded solve (tiled fill + exchange), all ranks",
                          "peak_model": "N x 148 SMs x sm_max_mhz x 21.33 transitions/clk/SM"},
             "cpu_baseline": None, "e2e": e2e,
+            "gpu_launches": launches,  # this library's kernels on rank 0 (NCCL's own are not counted)
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()

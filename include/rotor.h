@@ -182,6 +182,9 @@ int rotor_sharded_pack(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t t
 int rotor_sharded_finish(rotor_shard *h, void *stream, double *d_cost, rotor_op *d_ops, int64_t ops_cap,
                          int64_t *d_n_ops, int32_t *d_status);
 int rotor_sharded_free(rotor_shard *h);
+/* Kernels this shard has launched since rotor_sharded_begin (begin, steps,
+ * packs / unpacks, finish); host-side counter, no synchronisation. */
+int rotor_sharded_launches(const rotor_shard *h, int64_t *launches);
 
 /* Longest-processing-time partition of n_items weighted items over n_parts
  * parts (host helper for sharding independent solves across GPUs/ranks).

@@ -88,6 +88,7 @@ _lib.rotor_sharded_step.argtypes = [_vp, _i32, _i32, _i32, _vp]
 _lib.rotor_sharded_pack.argtypes = [_vp, _i32, _i32, _i32, _vp, _u64, _i32, _vp]
 _lib.rotor_sharded_finish.argtypes = [_vp, _vp, _vp, _vp, _i64, _vp, _vp]
 _lib.rotor_sharded_free.argtypes = [_vp]
+_lib.rotor_sharded_launches.argtypes = [_vp, _P(_i64)]
 _lib.rotor_release.argtypes = []
 _lib.rotor_last_error.restype = _c.c_char_p
 _lib.rotor_version.restype = _i32
@@ -99,7 +100,7 @@ EXPORTS = (
     "rotor_last_timings",
     "rotor_release", "rotor_last_error", "rotor_version",
     "rotor_tile_blocks", "rotor_tile_bytes", "rotor_sharded_begin", "rotor_sharded_step", "rotor_sharded_pack",
-    "rotor_sharded_finish", "rotor_sharded_free",
+    "rotor_sharded_finish", "rotor_sharded_free", "rotor_sharded_launches",
 )
 
 
@@ -339,6 +340,11 @@ class Shard:
         _check(_lib.rotor_sharded_finish(self.h, _stream_ptr(stream), int(out["cost"].data_ptr()),
                                          int(out["ops"].data_ptr()), cap, int(out["n_ops"].data_ptr()),
                                          int(out["status"].data_ptr())))
+
+    def launches(self) -> int:
+        n = _i64()
+        _check(_lib.rotor_sharded_launches(self.h, _c.byref(n)))
+        return int(n.value)
 
     def close(self):
         if getattr(self, "h", None):

@@ -593,6 +593,7 @@ struct rotor_shard {
     rotor::TiledCtx ctx;
     int device;
     cudaStream_t stream;
+    int64_t launches = 0;
 };
 
 int32_t rotor_tile_blocks(int32_t L) { return L < 1 ? 0 : rotor::tiled_nb(L + 1); }
@@ -633,6 +634,7 @@ int rotor_sharded_begin(const rotor_chain *d_chain, int32_t L, uint64_t mem_limi
     h->y = y;
     h->p = p;
     h->stream = st;
+    h->launches = 2;  // precompute, leaf
     CK(cudaGetDevice(&h->device));
     *out = h;
     return ROTOR_OK;
@@ -643,8 +645,9 @@ int rotor_sharded_step(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t t
     const int nb = rotor::tiled_nb(h->p.n);
     if (delta < 0 || delta >= nb || tile_lo < 0 || tile_hi > nb - delta || tile_lo > tile_hi)
         return fail(ROTOR_EINPUT, "bad tile range [%d,%d) at delta %d", tile_lo, tile_hi, delta);
-    if (rotor::tiled_delta(h->p, &h->ctx, delta, tile_lo, tile_hi, (cudaStream_t)stream) < 0)
-        return fail(ROTOR_EDEVICE, "tiled step failed");
+    const int nl = rotor::tiled_delta(h->p, &h->ctx, delta, tile_lo, tile_hi, (cudaStream_t)stream);
+    if (nl < 0) return fail(ROTOR_EDEVICE, "tiled step failed");
+    h->launches += nl;
     CK(cudaGetLastError());
     return ROTOR_OK;
 }
@@ -657,8 +660,15 @@ int rotor_sharded_pack(rotor_shard *h, int32_t delta, int32_t tile_lo, int32_t t
         return fail(ROTOR_EINPUT, "bad pack arguments");
     if (buf_bytes < (uint64_t)(tile_hi - tile_lo) * rotor::tiled_tile_bytes(h->p.S))
         return fail(ROTOR_ENOMEM, "pack buffer too small");
-    rotor::tiled_pack(h->p, delta, tile_lo, tile_hi, (double *)d_buf, unpack ? 1 : 0, (cudaStream_t)stream);
+    h->launches += rotor::tiled_pack(h->p, delta, tile_lo, tile_hi, (double *)d_buf, unpack ? 1 : 0,
+                                     (cudaStream_t)stream);
     CK(cudaGetLastError());
+    return ROTOR_OK;
+}
+
+int rotor_sharded_launches(const rotor_shard *h, int64_t *launches) {
+    if (!h || !launches) return fail(ROTOR_EINPUT, "NULL argument");
+    *launches = h->launches;
     return ROTOR_OK;
 }
 
@@ -686,6 +696,7 @@ int rotor_sharded_finish(rotor_shard *h, void *stream, double *d_cost, rotor_op 
     p.ops = d_ops;
     p.ops_cap = ops_cap < 0 ? 0 : ops_cap;
     rotor::launch_reconstruct(p, (cudaStream_t)stream);
+    h->launches += 1;
     CK(cudaGetLastError());
     return ROTOR_OK;
 }
