@@ -457,10 +457,11 @@ int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_ch
     for (int64_t q = 0; q < P; q++) h_order[q] = (int32_t)q;
     std::stable_sort(h_order.begin(), h_order.end(),
                      [&](int32_t x, int32_t y) { return Ls[h_pc[x]] > Ls[h_pc[y]]; });
-    // persistent k_batch CTAs (512 threads, 40 registers): three resident per SM
-    // (config 5: 1 per SM 86.4 ms, 2 59.0, 3 50.0; 256 threads x 6 62.6, x 7
-    // 60.6; 384 x 4 50.6; 128 x 12 91.2)
-    const int n_slots = (int)std::min<int64_t>(P, 3 * (int64_t)sms);
+    // persistent k_batch CTAs (512 threads, 32 registers): four resident per SM,
+    // a full SM of threads (config 5: 1 per SM 86.4 ms, 2 59.0, 3 50.0 at 40
+    // registers / 47.5 at 32, 4 44.6; 256 threads x 6 62.6, x 7 60.6; 384 x 4
+    // 50.6; 128 x 12 91.2)
+    const int n_slots = (int)std::min<int64_t>(P, 4 * (int64_t)sms);
     const size_t slot = rotor::batch_slot_bytes(L_max, slots);
     // one device allocation (library cache): descriptors, outputs, ops, then the slot pool
     size_t off = 0;

@@ -46,7 +46,7 @@ __host__ __device__ inline SlotLayout slot_layout(int L_max, int S) {
     return y;
 }
 
-__global__ void __launch_bounds__(512) k_batch(BatchArgs b) {
+__global__ void __launch_bounds__(512, 4) k_batch(BatchArgs b) {  // 4 resident per SM (rotor_abi.cu)
     __shared__ int prob;
     const SlotLayout y = slot_layout(b.L_max, b.S);
     char *slot = b.pool + (size_t)blockIdx.x * y.bytes;
