@@ -454,14 +454,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Wide pruned middle: items of 32 s x 32 t x 32 m; a warp = 32 consecutive m
-// of one 8 x 8 (s,t) register tile.  The fp32 boxes have 128-byte (A) and
-// 144-byte (C) rows — twice the row length of the 16-m items, half the row
-// requests per byte — and each lane keeps only bestf for its 64 cells in
-// registers; the exact fp64 running minimum lives in the partial rows of C
-// in global memory (the middle kernel is their first writer), touched only
-// by the rare exact passes, which recompute just the splits whose filter
-// fired (per-split mask OR-reduced over the warp).
+// Wide pruned middle (the default, DESIGN 5.2): items of 32 s x 32 t x 32 m;
+// a warp = 32 consecutive m of one 8 x 8 (s,t) register tile.  The fp32
+// boxes have 128-byte (A) and 144-byte (C) rows — twice the row length of the
+// 16-m items, half the row requests per byte — and each lane keeps only bestf
+// for its 64 cells in registers.  Per split: a coarse bound for the whole
+// 8 x 8 tile, then per 4 x 4 quadrant, then the per-cell filter; the splits
+// that can still improve some cell of the warp (mask OR-reduced over the
+// warp) are recomputed exactly and folded into the partial rows of C (set to
+// +inf when the item starts) with 64-bit atomic min.
 // ---------------------------------------------------------------------------
 constexpr int TMW = 32, TMBW = TMW + 4, RW = 8;
 template <int KC_, int STAGES_>
