@@ -42,7 +42,7 @@ def build(force: bool = False) -> str:
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         tmp = LIB + f".tmp{os.getpid()}"
         subprocess.check_call(
-            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+            ["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared",
              "-o", tmp, SRC, "-lm"]
         )
         os.replace(tmp, LIB)
@@ -63,6 +63,14 @@ def lib():
         L.oracle_free.argtypes = [ctypes.c_void_p]
         L.oracle_fill.argtypes = [ctypes.c_void_p]
         L.oracle_fill.restype = i32
+        L.oracle_fill_threads.argtypes = [ctypes.c_void_p, i32]
+        L.oracle_fill_threads.restype = i32
+        L.oracle_set_keep_d.argtypes = [ctypes.c_void_p, i32]
+        L.oracle_set_keep_d.restype = i32
+        L.oracle_table.argtypes = [ctypes.c_void_p]
+        L.oracle_table.restype = ctypes.c_void_p
+        L.oracle_max_threads.argtypes = []
+        L.oracle_max_threads.restype = i32
         L.oracle_cost.argtypes = [ctypes.c_void_p]
         L.oracle_cost.restype = d
         L.oracle_cell.argtypes = [ctypes.c_void_p, i32, i32, i64]
@@ -96,6 +104,11 @@ def _p(a, ct):
     return a.ctypes.data_as(ctypes.POINTER(ct))
 
 
+def max_threads() -> int:
+    """OpenMP threads the oracle would use by default (OMP_NUM_THREADS / nproc)."""
+    return int(lib().oracle_max_threads())
+
+
 def slots_of(x: int, M: int, S: int) -> int:
     return int(lib().oracle_slots_of(int(x), int(M), int(S)))
 
@@ -125,8 +138,10 @@ class OracleSolve:
     """One DP table for (chain, M, S) — Algorithm 1 then Algorithm 2."""
 
     def __init__(self, chain, mem_limit: int, slots: int, restricted: bool = False, fill: bool = True,
-                 window=None):
-        """window=(s0, t0): store and fill only the cells s0 <= s <= t <= t0 (same values)."""
+                 window=None, threads: int = 1, keep_d: bool = True):
+        """window=(s0, t0): store and fill only the cells s0 <= s <= t <= t0 (same values).
+        threads > 1: the cells of each diagonal are spread over OpenMP threads (bit-identical).
+        keep_d=False: do not store the fill's argmin table (Algorithm 2 needs only C)."""
         self.chain = chain
         self.L, self.n, self.S = chain.L, chain.L + 1, int(slots)
         self.M = int(mem_limit)
@@ -140,6 +155,9 @@ class OracleSolve:
         self.window = window
         if window is not None and lib().oracle_set_window(self.h, int(window[0]), int(window[1])) != 0:
             raise ValueError(f"bad window {window}")
+        if not keep_d and lib().oracle_set_keep_d(self.h, 0) != 0:
+            raise ValueError("oracle_set_keep_d failed")
+        self.threads = int(threads)
         self.filled = False
         if fill:
             self.fill()
@@ -150,7 +168,7 @@ class OracleSolve:
             self.h = None
 
     def fill(self):
-        if lib().oracle_fill(self.h) != 0:
+        if lib().oracle_fill_threads(self.h, self.threads) != 0:
             raise MemoryError("oracle_fill: out of memory")
         self.filled = True
         return self
@@ -203,6 +221,14 @@ class OracleSolve:
         D = np.empty((self.cells, self.S + 1), dtype=np.uint16)
         assert lib().oracle_export(self.h, _p(C, ctypes.c_double), _p(D, ctypes.c_uint16)) == 0
         return C, D
+
+    def table_view(self) -> np.ndarray:
+        """The filled C table itself (no copy), shape (cells, S+1); valid while self lives."""
+        ptr = lib().oracle_table(self.h)
+        if not ptr:
+            raise RuntimeError("table not filled")
+        buf = (ctypes.c_double * (self.cells * (self.S + 1))).from_address(ptr)
+        return np.frombuffer(buf, dtype=np.float64).reshape(self.cells, self.S + 1)
 
     def decision_table(self):
         D = np.empty((self.cells, self.S + 1), dtype=np.uint16)

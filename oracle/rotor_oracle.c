@@ -24,12 +24,21 @@
  * D (argmin) codes: k = s'-s in 1..d for an F_ck split, 0 for F_all / leaf,
  *   0xFFFF when C = +inf.
  *
- * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -shared -fPIC
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fopenmp -shared -fPIC
+ *
+ * Threads: oracle_fill_threads() runs the very same per-cell
+ * computation with the cells of one diagonal d spread over OpenMP threads.  The
+ * cells of a diagonal read only shorter diagonals and each cell's
+ * candidate loop is unchanged, so the table is bit-identical to oracle_fill's
+ * (tests/test_oracle_pins.py::test_threaded_fill_bit_identical).
  */
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 
 #define OR_FALL 0
 #define OR_FCK 1
@@ -55,6 +64,7 @@ typedef struct {
      * of the whole chain, so windowed values are bit-identical to full ones. */
     int s0, nw;
     int filled;
+    int keep_d; /* store the fill's argmin table D (default 1) */
     /* reconstruction output */
     int32_t *ops;
     int64_t ops_cap, ops_n;
@@ -158,6 +168,7 @@ oracle_ctx *oracle_new(int L, int S, const double *uf, const double *ub, const u
     c->s0 = 1;
     c->nw = n;
     c->cells = (int64_t)n * (n + 1) / 2;
+    c->keep_d = 1;
     return c;
 }
 
@@ -199,61 +210,112 @@ static double C_all(oracle_ctx *c, int s, int t, int64_t m)
  * fixed m the candidate order is exactly the one above, so the result is the
  * same as the literal per-cell loop.
  */
-int oracle_fill(oracle_ctx *c)
+/* One cell (s, t=s+d) of Eq. (2) for every m, into C (and D when kept).
+ * best/arg are caller-provided scratch rows of S+1 entries. */
+static void fill_cell(oracle_ctx *c, int s, int t, double *best, int *arg)
+{
+    const int S = c->S;
+    int64_t mn = MNULL(c, s, t), ma = MALL(c, s, t);
+    for (int m = 0; m <= S; m++) { best[m] = INFINITY; arg[m] = OR_NONE; }
+    /* C_1: min over s' of C_ck, only where m >= m_null(s,t) */
+    for (int sp = s + 1; sp <= t; sp++) {
+        for (int m = 0; m <= S; m++) {
+            if (m < mn) continue;
+            double v = C_ck(c, s, sp, t, m);
+            if (v < best[m]) { best[m] = v; arg[m] = sp - s; }
+        }
+    }
+    /* C_2: C_all where m >= m_all(s,t); not at s < t in restricted mode */
+    if (!c->restricted) {
+        for (int m = 0; m <= S; m++) {
+            if (m < ma) continue;
+            double v = C_all(c, s, t, m);
+            if (v < best[m]) { best[m] = v; arg[m] = 0; }
+        }
+    }
+    double *Cst = Cp(c, s, t);
+    for (int m = 0; m <= S; m++) Cst[m] = best[m]; /* Eq. (2): C = min(C_1, C_2) */
+    if (c->D) {
+        uint16_t *Dst = Dp(c, s, t);
+        for (int m = 0; m <= S; m++) Dst[m] = isinf(best[m]) ? OR_NONE : (uint16_t)arg[m];
+    }
+}
+
+/*
+ * Algorithm 1, with the fill order of Q3: by increasing d = t - s
+ * (Alg. 1's s-outer loop would read C[s',t] for s' > s before it is written).
+ * For each cell the candidates are visited in Alg. 2's order (Q11): F_ck with
+ * s' = s+1..t ascending under strict '<' (smallest s' wins a tie), then F_all
+ * only if strictly smaller.  The loop over m is innermost for speed; for every
+ * fixed m the candidate order is exactly the one above, so the result is the
+ * same as the literal per-cell loop.  nthreads > 1 spreads the independent
+ * cells of one diagonal over OpenMP threads (same per-cell arithmetic).
+ */
+int oracle_fill_threads(oracle_ctx *c, int nthreads)
 {
     const int S = c->S, W = S + 1;
     const int s_lo = c->s0, s_hi = c->s0 + c->nw - 1; /* window (whole chain by default) */
+    if (nthreads < 1) nthreads = 1;
     if (!c->C) {
         c->C = (double *)malloc((size_t)c->cells * W * sizeof(double));
-        c->D = (uint16_t *)malloc((size_t)c->cells * W * sizeof(uint16_t));
-        if (!c->C || !c->D) return -1;
+        if (!c->C) return -1;
+        if (c->keep_d) {
+            c->D = (uint16_t *)malloc((size_t)c->cells * W * sizeof(uint16_t));
+            if (!c->D) return -1;
+        }
     }
     /* Eq. (1): C[s,s,m] = uf[s] + ub[s] if m >= m_all(s,s) else +inf */
     for (int s = s_lo; s <= s_hi; s++) {
         double *Cs = Cp(c, s, s);
-        uint16_t *Ds = Dp(c, s, s);
         int64_t ma = MALL(c, s, s);
-        for (int m = 0; m <= S; m++) {
-            Cs[m] = (m >= ma) ? c->w[s] : INFINITY;
-            Ds[m] = (m >= ma) ? 0 : OR_NONE;
+        for (int m = 0; m <= S; m++) Cs[m] = (m >= ma) ? c->w[s] : INFINITY;
+        if (c->D) {
+            uint16_t *Ds = Dp(c, s, s);
+            for (int m = 0; m <= S; m++) Ds[m] = (m >= ma) ? 0 : OR_NONE;
         }
     }
-    double *best = (double *)malloc(W * sizeof(double));
-    int *arg = (int *)malloc(W * sizeof(int));
+    double *best = (double *)malloc((size_t)nthreads * W * sizeof(double));
+    int *arg = (int *)malloc((size_t)nthreads * W * sizeof(int));
     if (!best || !arg) { free(best); free(arg); return -1; }
     for (int d = 1; d <= s_hi - s_lo; d++) {
-        for (int s = s_lo; s + d <= s_hi; s++) {
-            int t = s + d;
-            int64_t mn = MNULL(c, s, t), ma = MALL(c, s, t);
-            for (int m = 0; m <= S; m++) { best[m] = INFINITY; arg[m] = OR_NONE; }
-            /* C_1: min over s' of C_ck, only where m >= m_null(s,t) */
-            for (int sp = s + 1; sp <= t; sp++) {
-                for (int m = 0; m <= S; m++) {
-                    if (m < mn) continue;
-                    double v = C_ck(c, s, sp, t, m);
-                    if (v < best[m]) { best[m] = v; arg[m] = sp - s; }
-                }
-            }
-            /* C_2: C_all where m >= m_all(s,t); not at s < t in restricted mode */
-            if (!c->restricted) {
-                for (int m = 0; m <= S; m++) {
-                    if (m < ma) continue;
-                    double v = C_all(c, s, t, m);
-                    if (v < best[m]) { best[m] = v; arg[m] = 0; }
-                }
-            }
-            double *Cst = Cp(c, s, t);
-            uint16_t *Dst = Dp(c, s, t);
-            for (int m = 0; m <= S; m++) {
-                Cst[m] = best[m]; /* Eq. (2): C = min(C_1, C_2) */
-                Dst[m] = isinf(best[m]) ? OR_NONE : (uint16_t)arg[m];
-            }
+        int n_cells = s_hi - d - s_lo + 1;
+#pragma omp parallel for num_threads(nthreads) schedule(dynamic, 1) if (nthreads > 1)
+        for (int i = 0; i < n_cells; i++) {
+            int tid = 0;
+#ifdef _OPENMP
+            tid = omp_get_thread_num();
+#endif
+            int s = s_lo + i;
+            fill_cell(c, s, s + d, best + (size_t)tid * W, arg + (size_t)tid * W);
         }
     }
     free(best);
     free(arg);
     c->filled = 1;
     return 0;
+}
+
+int oracle_fill(oracle_ctx *c) { return oracle_fill_threads(c, 1); }
+
+/* Keep (1, default) or drop (0) the fill's argmin table D; call before filling.
+ * Algorithm 2 (oracle_decision / oracle_reconstruct) needs only C. */
+int oracle_set_keep_d(oracle_ctx *c, int keep)
+{
+    if (c->filled || c->C) return -1;
+    c->keep_d = keep ? 1 : 0;
+    return 0;
+}
+
+/* Borrowed pointer to the filled C table (canonical layout, cells x (S+1)). */
+const double *oracle_table(const oracle_ctx *c) { return c->filled ? c->C : NULL; }
+
+int oracle_max_threads(void)
+{
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
 }
 
 int64_t oracle_m_top(const oracle_ctx *c) { return (int64_t)c->S - c->wx[0]; } /* Q5, Alg. 1 */
@@ -336,7 +398,7 @@ int64_t oracle_reconstruct(oracle_ctx *c, int s, int t, int64_t m, int32_t *ops,
 /* Export C (fp64) and D (uint16) in the canonical layout; either pointer may be NULL. */
 int oracle_export(oracle_ctx *c, double *C, uint16_t *D)
 {
-    if (!c->filled) return -1;
+    if (!c->filled || (D && !c->D)) return -1;
     size_t cnt = (size_t)c->cells * (c->S + 1);
     if (C) memcpy(C, c->C, cnt * sizeof(double));
     if (D) memcpy(D, c->D, cnt * sizeof(uint16_t));

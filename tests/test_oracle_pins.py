@@ -491,3 +491,109 @@ def test_window_mode_equals_full_table(oracle_mod):
                 a = C[O.cell_index(n, s, t)]
                 b = Cw[O.cell_index(nw, s - s0 + 1, t - s0 + 1)]
                 assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+# ---------------------------------------------------------------------------
+# §8(d)(ii): the all-core oracle is the same computation (bit-identical)
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("restricted", [False, True])
+def test_threaded_fill_bit_identical(oracle_mod, restricted):
+    """OpenMP over the cells of each diagonal (oracle_fill_threads) reproduces the
+    single-thread fill bit for bit (C and D), on config 2 and random tiny chains;
+    keep_d=False changes nothing in C."""
+    O = oracle_mod
+    cases = [(G.config2().chain, G.config2().mem_limit, G.config2().slots)]
+    rng = G.SplitMix64(77)
+    for _ in range(6):
+        ch = G.random_chain(rng, rng.randint(3, 40), real_times=True)
+        cases.append((ch, G.budget_ref(ch) // 3, 60))
+    for ch, M, S in cases:
+        a = _solve(O, ch, M, S, restricted=restricted)
+        for thr in (2, 5):
+            b = _solve(O, ch, M, S, restricted=restricted, threads=thr)
+            Ca, Da = a.tables()
+            Cb, Db = b.tables()
+            assert np.array_equal(Ca.view(np.uint64), Cb.view(np.uint64))
+            assert np.array_equal(Da, Db)
+        c = _solve(O, ch, M, S, restricted=restricted, threads=3, keep_d=False)
+        assert np.array_equal(Ca.view(np.uint64), c.table_view().view(np.uint64))
+        assert c.reconstruct() == a.reconstruct()
+
+
+def test_threaded_fill_window_config3(oracle_mod):
+    """A 120-stage window of config 3 (S=2000): threaded == single thread."""
+    O = oracle_mod
+    p = G.config3()
+    a = _solve(O, p.chain, p.mem_limit, p.slots, window=(90, 209), keep_d=False)
+    b = _solve(O, p.chain, p.mem_limit, p.slots, window=(90, 209), keep_d=False, threads=O.max_threads())
+    assert np.array_equal(a.table_view().view(np.uint64), b.table_view().view(np.uint64))
+
+
+# ---------------------------------------------------------------------------
+# checksum module of the full-size golden (tests/table_hash.py)
+# ---------------------------------------------------------------------------
+def test_table_hash_definition_and_sensitivity(oracle_mod):
+    """The vectorised checksums equal their definition written with Python ints,
+    and flipping any single bit of any value changes the checksum of its cell's
+    s and d (so the config-4 golden localises a mismatch)."""
+    import table_hash as TH
+
+    O = oracle_mod
+    p = G.config1()
+    o = _solve(O, p.chain, p.mem_limit, p.slots)
+    C = o.table_view().copy()
+    n = o.n
+    hs = TH.hash_canonical_table(C, n, chunk=7)
+    K = [int(x) for x in TH.row_keys(C.shape[1])]
+    K2 = [int(x) for x in TH.cell_keys(n)]
+    M = (1 << 64) - 1
+    H = [0] * (n + 1)
+    Gd = [0] * n
+    for s in range(1, n + 1):
+        for t in range(s, n + 1):
+            row = C[TH.cell_index(n, s, t)].view(np.uint64)
+            h = sum(int(b) * k for b, k in zip(row, K)) & M
+            H[s] = (H[s] + h * K2[t]) & M
+            Gd[t - s] = (Gd[t - s] + h * K2[s]) & M
+    assert [int(x) for x in hs.H] == H and [int(x) for x in hs.G] == Gd
+    rng = G.SplitMix64(3)
+    for _ in range(50):
+        s = rng.randint(1, n)
+        t = rng.randint(s, n)
+        m = rng.randint(0, C.shape[1] - 1)
+        bit = rng.randint(0, 63)
+        D = C.copy()
+        D.view(np.uint64)[TH.cell_index(n, s, t), m] ^= np.uint64(1 << bit)
+        h2 = TH.hash_canonical_table(D, n)
+        assert (h2.H != hs.H).sum() == 1 and h2.H[s] != hs.H[s]
+        assert (h2.G != hs.G).sum() == 1 and h2.G[t - s] != hs.G[t - s]
+
+
+def test_cfg4_golden_file_consistent():
+    """The committed config-4 golden (scripts/make_golden_cfg4.py, oracle only) is
+    well formed: cost = its top row at m_top, checksums for every s and d, and an
+    Algorithm-2 schedule with exactly one B per stage (P7)."""
+    import table_hash as TH
+
+    path = os.path.join(GOLDEN, "cfg4_L1000_S4000.txt")
+    g = TH.read_golden(path)
+    L, S, m_top = int(g["L"]), int(g["S"]), int(g["m_top"])
+    n = L + 1
+    assert len(g["top"]) == S + 1 and len(g["H"]) == n and len(g["G"]) == n
+    assert g["top"][m_top] == int(g["cost"], 16)
+    assert np.float64(float(g["cost_float"])).view(np.uint64) == np.uint64(int(g["cost"], 16))
+    ops = [(x >> 32, x & 0xFFFFFFFF) for x in g["ops"]]
+    assert len(ops) == int(g["n_ops"])
+    assert sorted(st for op, st in ops if op == 3) == list(range(1, n + 1))
+    top = np.array(g["top"], dtype=np.uint64).view(np.float64)
+    assert np.all(top[1:] <= top[:-1])  # P4 monotone in m
+    p = G.config4()
+    assert (L, S, int(g["M"])) == (p.chain.L, p.slots, p.mem_limit)
+    # P7: the schedule replays valid within the budget and reproduces the cost (Q14)
+    O = pytest.importorskip("oracle")
+    sz = O.OracleSolve(p.chain, p.mem_limit, p.slots, fill=False).sizes()
+    rep = O.simulate(ops, sz, S)
+    cost = float(g["cost_float"])
+    assert rep.valid, rep.failure
+    assert abs(rep.makespan - cost) <= len(ops) * math.ulp(cost)
+    assert cost >= float(np.sum(p.chain.uf) + np.sum(p.chain.ub)) * (1 - 1e-12)  # P5
