@@ -81,7 +81,8 @@ typedef struct {
     int32_t kernel;      /* rotor_kernel */
     int32_t keep_argmin; /* 1: record D (uint16 argmin) during the fill (wavefront kernel only) */
     int32_t profile;     /* 1: time the phases with CUDA events (see rotor_last_timings) */
-    int32_t reserved[4];
+    int32_t counters;    /* 1: count the pruned middle kernel's work (see rotor_last_counters) */
+    int32_t reserved[3];
 } rotor_options;
 
 /* Default options: all zero (unrestricted, auto kernel, no D, no profiling). */
@@ -226,6 +227,32 @@ typedef struct {
     int32_t middle_launches;
 } rotor_timings;
 int rotor_last_timings(rotor_timings *out);
+
+/* Work counters of the last solve on this thread (options.counters = 1, tiled
+ * fill).  Every cell of diagonal d >= 1 has d + 1 candidates (Eq. (2),
+ * P:723-737); the nominal count is independent of gating and pruning.  The
+ * tiled fill's middle kernel (splits s' in the tile blocks strictly between
+ * the cell's row and column blocks) filters its candidates
+ * with exact fp32 lower bounds; what it did is counted per (warp, split)
+ * visit, a warp covering an 8 x 8 cell tile x 32 m (2048 candidates):
+ *   middle_split_visits : (warp, split) visits            (x 2048 candidates)
+ *   coarse_pass         : visits whose whole-tile bound did not reject the split
+ *   quadrant_compares   : 4 x 4 quadrants compared cell by cell (x 512 fp32 compares)
+ *   exact_splits        : visits recomputed in fp64        (x 2048 candidates)
+ * Everything else (the dependent phase: splits inside the cell's own tile
+ * blocks, F_all, the gates) is evaluated exactly, candidate by candidate.
+ * Synchronous. */
+typedef struct {
+    double nominal;                 /* sum_{d=1}^{L} (n-d)(d+1)(S+1) */
+    double middle_nominal;          /* candidates of the middle ranges (existing cells, m = 0..S) */
+    double dependent_nominal;       /* nominal - middle_nominal */
+    uint64_t middle_split_visits;
+    uint64_t coarse_pass;
+    uint64_t quadrant_compares;
+    uint64_t exact_splits;
+    double evaluated;               /* 512 quadrant_compares + 2048 exact_splits + dependent_nominal */
+} rotor_counters;
+int rotor_last_counters(rotor_counters *out);
 
 /* Release the library-owned cached workspaces (all devices). */
 int rotor_release(void);

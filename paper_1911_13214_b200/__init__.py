@@ -47,7 +47,7 @@ class rotor_op(ctypes.Structure):
 class rotor_options(ctypes.Structure):
     _fields_ = [
         ("restricted", ctypes.c_int32), ("kernel", ctypes.c_int32), ("keep_argmin", ctypes.c_int32),
-        ("profile", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4),
+        ("profile", ctypes.c_int32), ("counters", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3),
     ]
 
 
@@ -56,6 +56,14 @@ class rotor_timings(ctypes.Structure):
         ("pre_ms", ctypes.c_double), ("fill_ms", ctypes.c_double), ("reconstruct_ms", ctypes.c_double),
         ("fill_launches", ctypes.c_int32), ("total_launches", ctypes.c_int32),
         ("middle_ms", ctypes.c_double), ("middle_launches", ctypes.c_int32),
+    ]
+
+
+class rotor_counters(ctypes.Structure):
+    _fields_ = [
+        ("nominal", ctypes.c_double), ("middle_nominal", ctypes.c_double), ("dependent_nominal", ctypes.c_double),
+        ("middle_split_visits", ctypes.c_uint64), ("coarse_pass", ctypes.c_uint64),
+        ("quadrant_compares", ctypes.c_uint64), ("exact_splits", ctypes.c_uint64), ("evaluated", ctypes.c_double),
     ]
 
 
@@ -79,6 +87,7 @@ _lib.rotor_transitions.argtypes = [_i32, _i32]
 _lib.rotor_transitions.restype = _d
 _lib.rotor_export_tables.argtypes = [_vp, _vp, _i64]
 _lib.rotor_last_timings.argtypes = [_P(rotor_timings)]
+_lib.rotor_last_counters.argtypes = [_P(rotor_counters)]
 _lib.rotor_export_rows.argtypes = [_vp, _vp, _i64, _vp]
 _lib.rotor_tile_blocks.argtypes = [_i32]
 _lib.rotor_tile_blocks.restype = _i32
@@ -97,7 +106,7 @@ _lib.rotor_version.restype = _i32
 EXPORTS = (
     "rotor_solve", "rotor_solve_ex", "rotor_solve_device", "rotor_workspace_bytes", "rotor_max_ops",
     "rotor_solve_batch", "rotor_partition_lpt", "rotor_transitions", "rotor_export_tables", "rotor_export_rows",
-    "rotor_last_timings",
+    "rotor_last_timings", "rotor_last_counters",
     "rotor_release", "rotor_last_error", "rotor_version",
     "rotor_tile_blocks", "rotor_tile_bytes", "rotor_sharded_begin", "rotor_sharded_step", "rotor_sharded_pack",
     "rotor_sharded_finish", "rotor_sharded_free", "rotor_sharded_launches",
@@ -120,8 +129,9 @@ def _check(r: int, allow=(OK,)):
     return r
 
 
-def _options(restricted=False, kernel="auto", keep_argmin=False, profile=False) -> rotor_options:
+def _options(restricted=False, kernel="auto", keep_argmin=False, profile=False, counters=False) -> rotor_options:
     o = rotor_options()
+    o.counters = 1 if counters else 0
     o.restricted = 1 if restricted else 0
     o.kernel = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)
     o.keep_argmin = 1 if keep_argmin else 0
@@ -255,6 +265,13 @@ def last_timings() -> dict:
     return dict(pre_ms=t.pre_ms, fill_ms=t.fill_ms, reconstruct_ms=t.reconstruct_ms,
                 fill_launches=t.fill_launches, total_launches=t.total_launches,
                 middle_ms=t.middle_ms, middle_launches=t.middle_launches)
+
+
+def last_counters() -> dict:
+    """Work counters of the last solve (options counters=True; include/rotor.h rotor_counters)."""
+    c = rotor_counters()
+    _check(_lib.rotor_last_counters(_c.byref(c)))
+    return {k: getattr(c, k) for k, _ in rotor_counters._fields_}
 
 
 def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=None, **opts):

@@ -47,7 +47,7 @@ struct Layout {
     int stack_cap = 0;
     int64_t ops_cap = 0;
     size_t off_wx, off_wbx, off_wy, off_of, off_ob, off_P, off_w, off_mnull, off_stack, off_res;
-    size_t off_chain, off_ops, off_C, off_D, off_A, off_C32, off_A32, off_tiled;
+    size_t off_chain, off_ops, off_C, off_D, off_A, off_C32, off_A32, off_tiled, off_ctr;
     size_t total = 0;
     bool has_D = false;
     bool has_A = false;
@@ -92,6 +92,7 @@ Layout make_layout(int L, int S, const rotor_options &o) {
     y.off_mnull = take((size_t)y.n * y.n * 4);
     y.off_stack = take((size_t)y.stack_cap * sizeof(int4));
     y.off_res = take(64);
+    y.off_ctr = take(64);
     y.off_chain = take(7 * al(n2 * 8));
     y.off_ops = take((size_t)y.ops_cap * sizeof(rotor_op));
     y.off_C = take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 8);
@@ -126,8 +127,10 @@ rotor::Problem make_problem(const Layout &y, char *ws, const rotor_options &o) {
     p.C = (double *)(ws + y.off_C) + rotor::kPad;  // column m = 0 of row 0
     p.D = y.has_D ? (uint16_t *)(ws + y.off_D) + rotor::kPad : nullptr;
     p.A = y.has_A ? (double *)(ws + y.off_A) + rotor::kPad : nullptr;
-    p.C32 = y.has_A ? (float *)(ws + y.off_C32) + rotor::kPad : nullptr;
-    p.A32 = y.has_A ? (float *)(ws + y.off_A32) + rotor::kPad : nullptr;
+    p.C32 = y.has_A ? (float *)(ws + y.off_C32) : nullptr;
+    p.A32 = y.has_A ? (float *)(ws + y.off_A32) : nullptr;
+    p.srows = y.cells + rotor::kPadRows;
+    p.counters = (y.has_A && o.counters) ? (unsigned long long *)(ws + y.off_ctr) : nullptr;
     p.flags = y.has_A ? (int *)(ws + y.off_tiled) : nullptr;
     p.res_cost = (double *)(ws + y.off_res);
     p.res_nops = (int64_t *)(ws + y.off_res + 8);
@@ -176,6 +179,7 @@ struct LastSolve {
     int fill_launches = 0, total_launches = 0;
     std::vector<cudaEvent_t> mid_ev;  // pairs around the tiled fill's middle launches
     int mid_n = 0;
+    bool counted = false;  // options.counters: p.counters holds this solve's middle counters
 };
 thread_local LastSolve g_last;
 
@@ -240,6 +244,8 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
     g_last.device = dev;
     g_last.stream = st;
     g_last.profiled = o.profile != 0;
+    g_last.counted = p.counters != nullptr;
+    if (p.counters) CK(cudaMemsetAsync(p.counters, 0, 64, st));
     if (o.profile) {
         int r = ensure_events();
         if (r) return r;
@@ -711,10 +717,16 @@ int rotor_export_rows(const int32_t *s, const int32_t *t, int64_t n_rows, double
     if (dev != g_last.device) CK(cudaSetDevice(g_last.device));
     CK(cudaStreamSynchronize(g_last.stream));
     const size_t row = (size_t)(y.S + 1);
-    for (int64_t r = 0; r < n_rows; r++) {
+    for (int64_t r = 0; r < n_rows; r++)
         if (s[r] < 1 || t[r] < s[r] || t[r] > y.n) return fail(ROTOR_EINPUT, "bad cell (%d,%d)", s[r], t[r]);
-        const double *src = g_last.p.C + rotor::cell_index(y.n, s[r], t[r]) * y.pitch;
-        CK(cudaMemcpy(C_host + r * row, src, row * 8, cudaMemcpyDeviceToHost));
+    // runs of consecutive cells (e.g. (s, t..t+k) in the s-major order) go in one 2-D copy
+    for (int64_t r = 0; r < n_rows;) {
+        const int64_t c0 = rotor::cell_index(y.n, s[r], t[r]);
+        int64_t k = 1;
+        while (r + k < n_rows && rotor::cell_index(y.n, s[r + k], t[r + k]) == c0 + k) k++;
+        CK(cudaMemcpy2D(C_host + r * row, row * 8, g_last.p.C + c0 * y.pitch, (size_t)y.pitch * 8, row * 8,
+                        (size_t)k, cudaMemcpyDeviceToHost));
+        r += k;
     }
     if (dev != g_last.device) CK(cudaSetDevice(dev));
     return ROTOR_OK;
@@ -741,6 +753,28 @@ int rotor_last_timings(rotor_timings *out) {
     }
     out->middle_ms = mid;
     out->middle_launches = g_last.mid_n;
+    return ROTOR_OK;
+}
+
+int rotor_last_counters(rotor_counters *out) {
+    if (!out) return fail(ROTOR_EINPUT, "out is NULL");
+    if (!g_last.valid || !g_last.counted) return fail(ROTOR_EINPUT, "last solve did not count (options.counters)");
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    if (dev != g_last.device) CK(cudaSetDevice(g_last.device));
+    unsigned long long c[4];
+    CK(cudaStreamSynchronize(g_last.stream));
+    CK(cudaMemcpy(c, g_last.p.counters, sizeof c, cudaMemcpyDeviceToHost));
+    if (dev != g_last.device) CK(cudaSetDevice(dev));
+    const Layout &y = g_last.y;
+    out->nominal = rotor_transitions(y.L, y.S);
+    out->middle_nominal = (double)rotor::tiled_middle_candidates(y.n) * (y.S + 1);
+    out->dependent_nominal = out->nominal - out->middle_nominal;
+    out->middle_split_visits = c[0];
+    out->coarse_pass = c[1];
+    out->quadrant_compares = c[2];
+    out->exact_splits = c[3];
+    out->evaluated = 512.0 * (double)c[2] + 2048.0 * (double)c[3] + out->dependent_nominal;
     return ROTOR_OK;
 }
 

@@ -37,9 +37,15 @@ struct Problem {
     uint16_t *D;  // nullable
     double *A;    // nullable: A(s,c,m) = fl(fl(P[c]-P[s-1]) + C(s,c,m)), row a_index(s,c) (tiled fill)
     int *flags;   // nullable: tiled fill's leaf look-back flags (tiled_extra_bytes)
-    // nullable (tiled fill): fp32 round-down shadows of C and A, same rows and
-    // pitch (in elements), read by the pruned middle kernel's lower-bound filter
+    // nullable (tiled fill): fp32 round-down shadows of C and A in the m-chunked
+    // layout of shadow_index() over srows rows, read by the pruned middle
+    // kernel's lower-bound filter.  C32 is stored PRE-SHIFTED by the shift of
+    // the cell's first stage: C32(s,t,m) = rd(C(s, t, m - wx[s-1])), +inf for
+    // m < wx[s-1] (the split operand C(s', t, m - wx[s'-1]) depends on s' only)
     float *C32, *A32;
+    int64_t srows;
+    // nullable: profile counters of the pruned middle (rotor_counters order)
+    unsigned long long *counters;
     // reconstruction / results
     int4 *stack;
     int32_t stack_cap;
@@ -71,15 +77,30 @@ __device__ __forceinline__ int m_null(const Problem &p, int s, int t) {
     return p.mnullT[(int64_t)(t - 1) * p.n + (s - 1)];
 }
 
-// Store a finished cell's C and A with their fp32 round-down shadows
-// (cvt.rm: a lower bound of the fp64 value, +inf stays +inf).
-__device__ __forceinline__ void store_final_c(const Problem &p, int64_t off, double c) {
-    p.C[off] = c;
-    if (p.C32) p.C32[off] = __double2float_rd(c);
+// fp32 shadow layout: the row is cut into chunks of kSW = 32 m; chunk q of all
+// rows is contiguous, so the 32 m of 32 consecutive rows — one operand box of
+// the pruned middle kernel — are ONE contiguous 4 KB block (one bulk copy, full
+// DRAM bursts) instead of 32 separate 128-byte row pieces.
+constexpr int kSW = 32;
+__host__ __device__ __forceinline__ int64_t shadow_index(int64_t srows, int64_t row, int m) {
+    return ((int64_t)(m >> 5) * srows + row) * kSW + (m & (kSW - 1));
 }
-__device__ __forceinline__ void store_final_a(const Problem &p, int64_t off, double a) {
-    p.A[off] = a;
-    if (p.A32) p.A32[off] = __double2float_rd(a);
+
+// Store a finished cell's C and A with their fp32 round-down shadows
+// (cvt.rm: a lower bound of the fp64 value, +inf stays +inf).  row = the
+// cell's table row, w = wx[s-1] of its first stage s (the pre-shift of C32):
+// the thread of m writes shadow column m + w, and column m with +inf when
+// m < w, so columns 0..S are all written once.
+__device__ __forceinline__ void store_final_c(const Problem &p, int64_t row, int m, int w, double c) {
+    p.C[row * p.pitch + m] = c;
+    if (p.C32) {
+        if (m + w <= p.S) p.C32[shadow_index(p.srows, row, m + w)] = __double2float_rd(c);
+        if (m < w) p.C32[shadow_index(p.srows, row, m)] = INFINITY;
+    }
+}
+__device__ __forceinline__ void store_final_a(const Problem &p, int64_t row, int m, double a) {
+    p.A[row * p.pitch + m] = a;
+    if (p.A32) p.A32[shadow_index(p.srows, row, m)] = __double2float_rd(a);
 }
 
 }  // namespace rotor

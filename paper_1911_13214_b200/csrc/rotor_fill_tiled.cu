@@ -92,6 +92,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// non-blocking: true once the phase with this parity has completed (acquire)
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
 __device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1, uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
@@ -271,223 +286,117 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Pruned middle on the fp32 shadow tables (16-m items; the wide variant below
-// is the default).  The leaf kernels store,
-// with every final C and A value, its round-down fp32 copy (store_final_*), so
-// the TMA ring carries only fp32 boxes (half the bytes of the fp64 boxes: six
-// 36 KB stages, five in flight) and there is nothing to convert on chip.
-// Per cell the thread keeps acc (exact fp64 running minimum) and bestf =
-// cvt_ru(acc) >= acc; a candidate fl64(a + b) can lower acc only if
-// fadd_rd(a32, b32) < bestf (a32 = cvt_rd(a) <= a, b32 <= b, so the fp32 sum
-// rounded down is <= a + b, and by monotone rounding <= fl64(a + b)).  The
-// filter is FADD.RM + FSETP.OR per candidate; a warp whose chunk has any
-// passing candidate recomputes it exactly from the fp64 tables in global
-// memory (on every non-gated cell the same values as the boxes: m - wx >= 0
-// there; gated cells' partials are never used, DESIGN Q6).  The result is
-// bit-identical to k_tile_middle.
+// Pruned middle (the default, DESIGN 5.2): items of 32 s x 32 t x 32 m; a warp
+// = 32 consecutive m of one 8 x 8 (s,t) register tile.  The operands stream as
+// fp32 round-down shadows: per split s' one A box A32(i0..i0+31, s'-1, m0..+31)
+// and one C box C32(s', j0..j0+31, m0..+31), where C32 is stored pre-shifted by
+// wx[s'-1] (store_final_c), so both boxes are 32 consecutive rows x the same
+// aligned 32 m — in the m-chunked shadow layout (shadow_index) one contiguous
+// 4 KB block each, moved by one bulk copy (cp.async.bulk) into a full/empty
+// mbarrier ring.  Each lane keeps only bestf (>= the exact partial minimum)
+// for its 64 cells.  Per split: a coarse bound for the whole 8 x 8 tile, then
+// per 4 x 4 quadrant, then the per-cell filter fadd_rd(a32, b32) < bestf; the
+// splits that can still improve some cell of the warp (mask OR-reduced over
+// the warp) are recomputed exactly from the fp64 tables and folded into the
+// partial rows of C: the first candidate of a cell is stored, later ones go in
+// with a 64-bit atomic min, and the cells that never fired get +inf at the end
+// of the item (every partial is written once, no read back).
 // ---------------------------------------------------------------------------
-constexpr int TMB32 = TM + 4;  // fp32 C box: 16-byte aligned start column, offset 0..3
-struct F32Ring {
-    static constexpr int KC = 8, STAGES = 6;
-    static constexpr int A_ST = KC * TB * TM, B_ST = KC * TB * TMB32;  // floats per stage
-    static constexpr size_t bytes = (size_t)STAGES * (A_ST + B_ST) * 4 + 2 * STAGES * 8 + STAGES * KC * 4 + 64;
-};
-constexpr int F32_WX_MAX = (int)((227 * 1024 - F32Ring::bytes) / 4);
+constexpr int TMW = kSW, RW = 8;
+constexpr int BOX = TB * TMW;                    // floats per operand box (4 KB)
+constexpr int FMAX_CAP = 2048;                   // fired splits a warp can record per item (see fmax)
 
-__global__ void __launch_bounds__(THREADS, 1)
-    k_tile_middle_f32(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmC32,
-                      Problem p, int delta, int tile_lo, int n_tiles) {
-    using R = F32Ring;
-    constexpr int KC = R::KC, STAGES = R::STAGES, A_ST = R::A_ST, B_ST = R::B_ST;
-    extern __shared__ __align__(1024) float fsm[];
-    float *Af = fsm;                     // [STAGES][KC][TB s][TM]
-    float *Bf = Af + STAGES * A_ST;      // [STAGES][KC][TB t][TMB32]
-    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + STAGES * B_ST);
-    uint64_t *empty = full + STAGES;
-    int *soff = reinterpret_cast<int *>(empty + STAGES);  // [STAGES][KC]
-    int *wx_s = soff + STAGES * KC;
-
+// Exact pass of a warp over the splits it recorded for one item: s' = sp_lo +
+// flist[f], f < nf — or, if the list overflowed (nf > fmax), every split
+// sp_lo .. sp_lo + n_all - 1.  Every cell's candidates fl(A(s, s'-1, m) +
+// C(s', t, m - wx[s'-1])) (Q12) from the fp64 tables are min-ed and the
+// partial is stored once (+inf if no candidate).  Each (s, t, m) partial
+// belongs to exactly one lane, so nothing is atomic.  Rows in pairs keep the
+// running minima in 32 registers.
+__device__ __forceinline__ void exact_flush(const Problem &p, const uint16_t *flist, int nf, int fmax, int sp_lo,
+                                            int n_all, int s_0, int t_0, int m, int mc, const int *wxp) {
+    constexpr int RW = 8, RH = 2;
     const int n = p.n;
-    const int n_mc = (p.S + 1 + TM - 1) / TM;
-    const int n_items = n_tiles * n_mc;
-    if ((int)blockIdx.x >= n_items) return;
-    const int my_items = (n_items - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
-    const int iters = (delta - 1) * TB / KC;
-    const int total = my_items * iters;
-    const int tid = threadIdx.x;
-    const int lane = tid & 31;
-    const int *wxp = p.wx;
-    if (n <= F32_WX_MAX) {
-        for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
-        wxp = wx_s;
-    }
-    auto coords = [&](int gi, int &i0, int &j0, int &m0, int &sp0) {
-        const int item = (int)blockIdx.x + (gi / iters) * (int)gridDim.x;
-        const int I = tile_lo + item / n_mc, J = I + delta;
-        i0 = I * TB + 1;
-        j0 = J * TB + 1;
-        m0 = (item % n_mc) * TM;
-        sp0 = i0 + TB + (gi % iters) * KC;
-    };
-    auto issue = [&](int gi) {
-        const int st = gi % STAGES;
-        int i0, j0, m0, sp0;
-        coords(gi, i0, j0, m0, sp0);
-        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 3;
-        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 4));
-        for (int k = 0; k < KC; k++)
-            tma_load_2d(Af + st * A_ST + k * TB * TM, &tmA32, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
-        for (int k = 0; k < KC; k++) {
-            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
-            tma_load_2d(Bf + st * B_ST + k * TB * TMB32, &tmC32, c0 & ~3, (int)cell_index(n, sp0 + k, j0),
-                        &full[st]);
+    if (m > p.S) return;
+    const bool all = nf > fmax;
+    const int cnt = all ? n_all : nf;
+#pragma unroll 1
+    for (int h = 0; h < RW / RH; h++) {
+        double acc[RH][RW];
+#pragma unroll
+        for (int i = 0; i < RH; i++)
+#pragma unroll
+            for (int j = 0; j < RW; j++) acc[i][j] = INFINITY;
+#pragma unroll 1
+        for (int f = 0; f < cnt; f++) {
+            const int sp = sp_lo + (all ? f : (int)flist[f]);
+            const int mm = mc - wxp[sp - 1];
+            const double *ap = p.A + a_index(s_0 + RH * h, sp - 1) * p.pitch + mc;
+            const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
+            double ad[RH], bd[RW];
+#pragma unroll
+            for (int i = 0; i < RH; i++) ad[i] = __ldcg(ap + (int64_t)i * p.pitch);
+#pragma unroll
+            for (int j = 0; j < RW; j++) bd[j] = (mm >= 0 && t_0 + j <= n) ? __ldcg(bp + (int64_t)j * p.pitch) : INFINITY;
+#pragma unroll
+            for (int i = 0; i < RH; i++)
+#pragma unroll
+                for (int j = 0; j < RW; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(ad[i], bd[j]));
         }
-    };
-    if (tid == 0) {
-        for (int s = 0; s < STAGES; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CONSUMERS / 32);
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    }
-    __syncthreads();
-    constexpr int PRODUCER = CONSUMERS - 32;
-    if (tid == PRODUCER)
-        for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);
-
-    const int mi = tid & 15;
-    const int g = tid >> 4;
-    const int sg = g / (TB / RT), tg = g % (TB / RT);
-    for (int kl = 0; kl < my_items; kl++) {
-        double acc[RS][RT];
-        // bestf = cvt_ru(acc) >= acc; -inf (never passes the filter) on the
-        // cells whose partial is never used: gated (m < m_null(s,t), P:726 —
-        // the C operand there can come from a clamped box or a pad, DESIGN
-        // Q6), t > n, and m > S
-        float bestf[RS][RT];
-        {
-            const int item = (int)blockIdx.x + kl * (int)gridDim.x;
-            const int I = tile_lo + item / n_mc, J = I + delta;
-            const int s_0 = I * TB + 1 + sg * RS, t_0 = J * TB + 1 + tg * RT;
-            const int m = (item % n_mc) * TM + mi;
 #pragma unroll
-            for (int i = 0; i < RS; i++)
+        for (int i = 0; i < RH; i++) {
+            double *crow = p.C + cell_index(n, s_0 + RH * h + i, min(t_0, n)) * p.pitch + m;
 #pragma unroll
-                for (int j = 0; j < RT; j++) {
-                    acc[i][j] = INFINITY;
-                    const int t = t_0 + j;
-                    bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + i, t)) ? INFINITY : -INFINITY;
-                }
-        }
-        for (int it = 0; it < iters; it++) {
-            const int gi = kl * iters + it;
-            const int st = gi % STAGES;
-            mbar_wait(&full[st], (uint32_t)((gi / STAGES) & 1));
-            bool need = false;
-            {
-                const float *a_f = Af + st * A_ST + (sg * RS) * TM + mi;
-                const float *b_f = Bf + st * B_ST + (tg * RT) * TMB32 + mi;
-#pragma unroll
-                for (int k = 0; k < KC; k++) {
-                    float a[RS], b[RT];
-                    const float *bk = b_f + k * TB * TMB32 + soff[st * KC + k];
-#pragma unroll
-                    for (int i = 0; i < RS; i++) a[i] = a_f[k * TB * TM + i * TM];
-#pragma unroll
-                    for (int j = 0; j < RT; j++) b[j] = bk[j * TMB32];
-#pragma unroll
-                    for (int i = 0; i < RS; i++)
-#pragma unroll
-                        for (int j = 0; j < RT; j++) need |= __fadd_rd(a[i], b[j]) < bestf[i][j];
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            if (tid == PRODUCER && gi + STAGES < total) {
-                mbar_wait(&empty[st], (uint32_t)((gi / STAGES) & 1));
-                issue(gi + STAGES);
-            }
-            if (__any_sync(0xffffffffu, need)) {  // exact fp64 chunk, operands from global memory
-                int i0, j0, m0, sp0;
-                coords(gi, i0, j0, m0, sp0);
-                const int m = min(m0 + mi, p.S);
-                const int s_0 = i0 + sg * RS, t_0 = j0 + tg * RT;
-#pragma unroll 2
-                for (int k = 0; k < KC; k++) {
-                    const int sp = sp0 + k;
-                    const int mm = m - wxp[sp - 1];
-                    double a[RS], b[RT];
-                    const double *ap = p.A + a_index(s_0, sp - 1) * p.pitch + m;
-#pragma unroll
-                    for (int i = 0; i < RS; i++) a[i] = __ldcg(ap + (int64_t)i * p.pitch);
-                    const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
-#pragma unroll
-                    for (int j = 0; j < RT; j++)
-                        b[j] = (mm >= 0 && t_0 + j <= n) ? __ldcg(bp + (int64_t)j * p.pitch) : INFINITY;
-#pragma unroll
-                    for (int i = 0; i < RS; i++)
-#pragma unroll
-                        for (int j = 0; j < RT; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[i], b[j]));
-                }
-#pragma unroll
-                for (int i = 0; i < RS; i++)
-#pragma unroll
-                    for (int j = 0; j < RT; j++) bestf[i][j] = __double2float_ru(acc[i][j]);
-            }
-        }
-        const int item = (int)blockIdx.x + kl * (int)gridDim.x;
-        const int I = tile_lo + item / n_mc, J = I + delta;
-        const int i0 = I * TB + 1, j0 = J * TB + 1;
-        const int m = (item % n_mc) * TM + mi;
-        if (m <= p.S) {
-#pragma unroll
-            for (int i = 0; i < RS; i++) {
-                const int s = i0 + sg * RS + i;
-#pragma unroll
-                for (int j = 0; j < RT; j++) {
-                    const int t = j0 + tg * RT + j;
-                    if (t <= n) p.C[cell_index(n, s, t) * p.pitch + m] = acc[i][j];
-                }
-            }
+            for (int j = 0; j < RW; j++)
+                if (t_0 + j <= n) crow[(int64_t)j * p.pitch] = acc[i][j];
         }
     }
 }
 
-// ---------------------------------------------------------------------------
-// Wide pruned middle (the default, DESIGN 5.2): items of 32 s x 32 t x 32 m;
-// a warp = 32 consecutive m of one 8 x 8 (s,t) register tile.  The fp32
-// boxes have 128-byte (A) and 144-byte (C) rows — twice the row length of the
-// 16-m items, half the row requests per byte — and each lane keeps only bestf
-// for its 64 cells in registers.  Per split: a coarse bound for the whole
-// 8 x 8 tile, then per 4 x 4 quadrant, then the per-cell filter; the splits
-// that can still improve some cell of the warp (mask OR-reduced over the
-// warp) are recomputed exactly and folded into the partial rows of C (set to
-// +inf when the item starts) with 64-bit atomic min.
-// ---------------------------------------------------------------------------
-constexpr int TMW = 32, TMBW = TMW + 4, RW = 8;
 template <int KC_, int STAGES_>
 struct WideRing {
     static constexpr int KC = KC_, STAGES = STAGES_;
-    static constexpr int A_ST = KC * TB * TMW, B_ST = KC * TB * TMBW;  // floats per stage
-    static constexpr size_t bytes = (size_t)STAGES * (A_ST + B_ST) * 4 + 2 * STAGES * 8 + STAGES * KC * 4 + 64;
+    static constexpr int ST = 2 * KC * BOX;  // floats per stage: KC A boxes, then KC C boxes
+    // + the fired-split lists: NWARPS x fmax uint16 (wide_list_bytes)
+    static constexpr size_t bytes = (size_t)STAGES * ST * 4 + 2 * STAGES * 8 + STAGES * 4 + 64;
 };
+// fired-split list length per warp: every split of the longest item
+// ((nb - 2) * TB), capped by FMAX_CAP and by the shared memory left next to
+// the ring and wx (a longer list overflows into an all-splits exact pass)
+inline int wide_fmax(int n, size_t ring_bytes) {
+    const size_t wx_b = n <= 4096 ? (size_t)n * 4 : 0;
+    const int room = (int)((227 * 1024 - ring_bytes - wx_b) / ((CONSUMERS / 32) * 2)) & ~7;
+    return max(8, min(min(FMAX_CAP, room), max(1, ((n + TB - 1) / TB - 2) * TB)));
+}
 constexpr int WKC = 4, WSTAGES = 4;  // ring of the wide middle (see tiled_delta)
-constexpr int WIDE_WX_MAX = (int)((227 * 1024 - WideRing<WKC, WSTAGES>::bytes) / 4);
+constexpr int WIDE_WX_MAX = 4096;  // wx staged in shared memory up to this n (wide_fmax agrees)
+__host__ __device__ inline bool n_wx_smem(int n) { return n <= WIDE_WX_MAX; }
 static_assert((TB / RW) * (TB / RW) * TMW == THREADS, "one lane per (m, 8x8 tile)");
 
-template <int KCW, int STG>
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// profile counters (Problem::counters, rotor_counters order)
+enum { CTR_SPLITS = 0, CTR_COARSE_PASS = 1, CTR_QUADS = 2, CTR_EXACT = 3, CTR_N = 4 };
+
+template <int KCW, int STG, bool COUNT>
 __global__ void __launch_bounds__(THREADS, 1)
-    k_tile_middle_wide(const __grid_constant__ CUtensorMap tmA32, const __grid_constant__ CUtensorMap tmC32,
-                       Problem p, int delta, int tile_lo, int n_tiles, int coarse) {
+    k_tile_middle_wide(Problem p, int delta, int tile_lo, int n_tiles, int coarse, int fmax) {
     using R = WideRing<KCW, STG>;
-    constexpr int KC = R::KC, STAGES = R::STAGES, A_ST = R::A_ST, B_ST = R::B_ST;
+    constexpr int KC = R::KC, STAGES = R::STAGES, ST = R::ST;
+    constexpr int NWARPS = CONSUMERS / 32;
     extern __shared__ __align__(1024) float fsm[];
-    float *Af = fsm;                 // [STAGES][KC][TB s][TMW]
-    float *Bf = Af + STAGES * A_ST;  // [STAGES][KC][TB t][TMBW]
-    uint64_t *full = reinterpret_cast<uint64_t *>(Bf + STAGES * B_ST);
+    float *ring = fsm;  // [STAGES][A: KC][TB s][TMW] [C: KC][TB t][TMW]
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring + STAGES * ST);
     uint64_t *empty = full + STAGES;
-    int *soff = reinterpret_cast<int *>(empty + STAGES);  // [STAGES][KC]
-    int *wx_s = soff + STAGES * KC;
+    int *claim = reinterpret_cast<int *>(empty + STAGES);  // step whose refill of the stage is still unclaimed
+    int *wx_s = claim + STAGES;                            // wx[0..n) when n <= WIDE_WX_MAX
+    uint16_t *fl_s = reinterpret_cast<uint16_t *>(wx_s + (n_wx_smem(p.n) ? p.n : 0));  // [NWARPS][fmax]
 
     const int n = p.n;
     const int n_mc = (p.S + 1 + TMW - 1) / TMW;
@@ -499,7 +408,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int tid = threadIdx.x;
     const int lane = tid & 31, warp = tid >> 5;
     const int *wxp = p.wx;
-    if (n <= WIDE_WX_MAX) {
+    if (n_wx_smem(n)) {
         for (int i = tid; i < n; i += THREADS) wx_s[i] = p.wx[i];
         wxp = wx_s;
     }
@@ -515,29 +424,30 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int st = gi % STAGES;
         int i0, j0, m0, sp0;
         coords(gi, i0, j0, m0, sp0);
-        for (int k = 0; k < KC; k++) soff[st * KC + k] = (max(m0 - wxp[sp0 + k - 1], -kPad) + kPad) & 3;
-        mbar_expect_tx(&full[st], (uint32_t)((A_ST + B_ST) * 4));
-        for (int k = 0; k < KC; k++)
-            tma_load_2d(Af + st * A_ST + k * TB * TMW, &tmA32, m0 + kPad, (int)a_index(i0, sp0 + k - 1), &full[st]);
-        for (int k = 0; k < KC; k++) {
-            const int c0 = max(m0 - wxp[sp0 + k - 1], -kPad) + kPad;
-            tma_load_2d(Bf + st * B_ST + k * TB * TMBW, &tmC32, c0 & ~3, (int)cell_index(n, sp0 + k, j0),
-                        &full[st]);
-        }
+        mbar_expect_tx(&full[st], (uint32_t)(ST * 4));
+        float *dst = ring + st * ST;
+        for (int k = 0; k < KC; k++)  // A32(i0..i0+31, sp-1, m0..m0+31): rows a_index(i0.., sp-1) are consecutive
+            bulk_load(dst + k * BOX, p.A32 + shadow_index(p.srows, a_index(i0, sp0 + k - 1), m0), BOX * 4, &full[st]);
+        for (int k = 0; k < KC; k++)  // C32(sp, j0..j0+31, m0..): rows cell_index(sp, j0..) are consecutive
+            bulk_load(dst + (KC + k) * BOX, p.C32 + shadow_index(p.srows, cell_index(n, sp0 + k, j0), m0), BOX * 4,
+                      &full[st]);
     };
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], CONSUMERS / 32);
+            mbar_init(&empty[s], NWARPS);
+            claim[s] = s;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
-    constexpr int PRODUCER = CONSUMERS - 32;
-    if (tid == PRODUCER)
+    if (tid == 0)
         for (int gi = 0; gi < STAGES && gi < total; gi++) issue(gi);
+    __syncwarp();
 
+    unsigned c_coarse = 0, c_quads = 0, c_exact = 0;  // profile counters (warp-uniform, COUNT only)
     const int sg = warp / (TB / RW), tg = warp % (TB / RW);
+    uint16_t *flist = fl_s + warp * fmax;  // this warp's fired splits of the current item (s' - sp_lo)
     for (int kl = 0; kl < my_items; kl++) {
         const int item = (int)blockIdx.x + kl * (int)gridDim.x;
         const int I = tile_lo + item / n_mc, J = I + delta;
@@ -565,115 +475,106 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int j = 4 * qb; j < 4 * qb + 4; j++) maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
             }
-        // the partial rows start at +inf; the rare exact passes fold their
-        // candidates in with 64-bit atomic min (RED, nothing read back: every
-        // value is >= 0 or +inf, so the fp64 order is the uint64 order, Q13)
-        if (m <= p.S) {
-#pragma unroll 1
-            for (int i = 0; i < RW; i++) {
-                double *crow = p.C + cell_index(n, s_0 + i, min(t_0, n)) * p.pitch + m;
-#pragma unroll
-                for (int j = 0; j < RW; j++)
-                    if (t_0 + j <= n) crow[(int64_t)j * p.pitch] = INFINITY;
-            }
-        }
+        int nf = 0;  // fired splits of this item (warp-uniform; > fmax: the list overflowed)
         for (int it = 0; it < iters; it++) {
             const int gi = kl * iters + it;
             const int st = gi % STAGES;
             mbar_wait(&full[st], (uint32_t)((gi / STAGES) & 1));
+            const float *a_f = ring + st * ST + (sg * RW) * TMW + lane;
+            const float *b_f = ring + st * ST + KC * BOX + (tg * RW) * TMW + lane;
             unsigned needk = 0;
-            {
-                const float *a_f = Af + st * A_ST + (sg * RW) * TMW + lane;
-                const float *b_f = Bf + st * B_ST + (tg * RW) * TMBW + lane;
 #pragma unroll 1
-                for (int k = 0; k < KC; k++) {
-                    float a[RW], b[RW];
-                    const float *bk = b_f + k * TB * TMBW + soff[st * KC + k];
+            for (int k = 0; k < KC; k++) {
+                float a[RW], b[RW];
 #pragma unroll
-                    for (int i = 0; i < RW; i++) a[i] = a_f[k * TB * TMW + i * TMW];
+                for (int i = 0; i < RW; i++) a[i] = a_f[k * BOX + i * TMW];
 #pragma unroll
-                    for (int j = 0; j < RW; j++) b[j] = bk[j * TMBW];
-                    // coarse bounds first: per 4 x 4 quadrant (qa, qb) of the lane's
-                    // tile, fadd_rd(min a over its rows, min b over its columns) is
-                    // <= every lb of the quadrant (monotone rounding) and maxq >= every
-                    // bestf of it; a quadrant is compared cell by cell only if that
-                    // bound is below maxq on some lane of the warp
-                    float ma[2], mb[2];
+                for (int j = 0; j < RW; j++) b[j] = b_f[k * BOX + j * TMW];
+                // coarse bounds first: per 4 x 4 quadrant (qa, qb) of the lane's
+                // tile, fadd_rd(min a over its rows, min b over its columns) is
+                // <= every lb of the quadrant (monotone rounding) and maxq >= every
+                // bestf of it; a quadrant is compared cell by cell only if that
+                // bound is below maxq on some lane of the warp
+                float ma[2], mb[2];
 #pragma unroll
-                    for (int h = 0; h < 2; h++) {
-                        ma[h] = fminf(fminf(a[4 * h], a[4 * h + 1]), fminf(a[4 * h + 2], a[4 * h + 3]));
-                        mb[h] = fminf(fminf(b[4 * h], b[4 * h + 1]), fminf(b[4 * h + 2], b[4 * h + 3]));
-                    }
-                    bool nk = false;
-                    const float mall = fmaxf(fmaxf(maxq[0][0], maxq[0][1]), fmaxf(maxq[1][0], maxq[1][1]));
-                    if (__any_sync(0xffffffffu, !coarse || __fadd_rd(fminf(ma[0], ma[1]), fminf(mb[0], mb[1])) < mall)) {
+                for (int h = 0; h < 2; h++) {
+                    ma[h] = fminf(fminf(a[4 * h], a[4 * h + 1]), fminf(a[4 * h + 2], a[4 * h + 3]));
+                    mb[h] = fminf(fminf(b[4 * h], b[4 * h + 1]), fminf(b[4 * h + 2], b[4 * h + 3]));
+                }
+                bool nk = false;
+                const float mall = fmaxf(fmaxf(maxq[0][0], maxq[0][1]), fmaxf(maxq[1][0], maxq[1][1]));
+                if (__any_sync(0xffffffffu, !coarse || __fadd_rd(fminf(ma[0], ma[1]), fminf(mb[0], mb[1])) < mall)) {
+                    if (COUNT) c_coarse++;
 #pragma unroll
-                        for (int qa = 0; qa < 2; qa++)
+                    for (int qa = 0; qa < 2; qa++)
 #pragma unroll
-                            for (int qb = 0; qb < 2; qb++) {
-                                const bool maybe = !coarse || __fadd_rd(ma[qa], mb[qb]) < maxq[qa][qb];
-                                if (__any_sync(0xffffffffu, maybe)) {
+                        for (int qb = 0; qb < 2; qb++) {
+                            const bool maybe = !coarse || __fadd_rd(ma[qa], mb[qb]) < maxq[qa][qb];
+                            if (__any_sync(0xffffffffu, maybe)) {
+                                if (COUNT) c_quads++;
 #pragma unroll
-                                    for (int i = 4 * qa; i < 4 * qa + 4; i++)
+                                for (int i = 4 * qa; i < 4 * qa + 4; i++)
 #pragma unroll
-                                        for (int j = 4 * qb; j < 4 * qb + 4; j++)
-                                            nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
-                                }
+                                    for (int j = 4 * qb; j < 4 * qb + 4; j++)
+                                        nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
                             }
-                    }
-                    needk |= (unsigned)nk << k;
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[st]);
-            if (tid == PRODUCER && gi + STAGES < total) {
-                mbar_wait(&empty[st], (uint32_t)((gi / STAGES) & 1));
-                issue(gi + STAGES);
-            }
-            needk = __reduce_or_sync(0xffffffffu, needk);
-            if (needk) {  // exact fp64 splits: operands from global memory, one round trip per split
-                int i0, j0, m0, sp0;
-                coords(gi, i0, j0, m0, sp0);
-#pragma unroll 1
-                for (int k = 0; k < KC; k++) {
-                    if (!((needk >> k) & 1)) continue;
-                    const int sp = sp0 + k;
-                    const int mm = mc - wxp[sp - 1];
-                    const double *ap = p.A + a_index(s_0, sp - 1) * p.pitch + mc;
-                    const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
-                    double ad[RW], bd[RW];
-#pragma unroll
-                    for (int i = 0; i < RW; i++) ad[i] = __ldcg(ap + (int64_t)i * p.pitch);
-#pragma unroll
-                    for (int j = 0; j < RW; j++)
-                        bd[j] = (mm >= 0 && t_0 + j <= n) ? __ldcg(bp + (int64_t)j * p.pitch) : INFINITY;
-#pragma unroll
-                    for (int i = 0; i < RW; i++) {
-                        unsigned long long *crow = reinterpret_cast<unsigned long long *>(
-                            p.C + cell_index(n, s_0 + i, min(t_0, n)) * p.pitch + mc);
-#pragma unroll
-                        for (int j = 0; j < RW; j++) {
-                            const double v = __dadd_rn(ad[i], bd[j]);
-                            if (t_0 + j <= n && m <= p.S && v < INFINITY)
-                                atomicMin(crow + (int64_t)j * p.pitch, (unsigned long long)__double_as_longlong(v));
-                            // bestf stays >= the running minimum: min(old bound, ru(v))
-                            bestf[i][j] = fminf(bestf[i][j], __double2float_ru(v));
                         }
-                    }
                 }
+                if (__any_sync(0xffffffffu, nk)) {
+                    // The split may lower some cell: it is recorded for the exact fp64
+                    // pass (deferred to the end of the item, so the warp does not stall
+                    // on global memory here), and every bestf drops to an fp32 UPPER
+                    // bound of the candidate the exact pass will evaluate: a <= nu(a32)
+                    // (a32 = rd(a), nu = next float up), so fl64(a + b) <= ru32(nu(a32)
+                    // + nu(b32)).  bestf then stays >= the final exact minimum.
+                    if (COUNT) c_exact++;
+                    const int q = nf + __popc(needk);
+                    if (lane == 0 && q < fmax) flist[q] = (uint16_t)(it * KC + k);  // s' - sp_lo
+                    float au[RW], bu[RW];
 #pragma unroll
-                for (int qa = 0; qa < 2; qa++)
+                    for (int i = 0; i < RW; i++) au[i] = __int_as_float(__float_as_int(a[i]) + (a[i] < INFINITY));
 #pragma unroll
-                    for (int qb = 0; qb < 2; qb++) {
-                        maxq[qa][qb] = -INFINITY;
+                    for (int j = 0; j < RW; j++) bu[j] = __int_as_float(__float_as_int(b[j]) + (b[j] < INFINITY));
 #pragma unroll
-                        for (int i = 4 * qa; i < 4 * qa + 4; i++)
+                    for (int i = 0; i < RW; i++)
 #pragma unroll
-                            for (int j = 4 * qb; j < 4 * qb + 4; j++)
-                                maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
-                    }
+                        for (int j = 0; j < RW; j++) bestf[i][j] = fminf(bestf[i][j], __fadd_ru(au[i], bu[j]));
+#pragma unroll
+                    for (int qa = 0; qa < 2; qa++)
+#pragma unroll
+                        for (int qb = 0; qb < 2; qb++) {
+                            maxq[qa][qb] = -INFINITY;
+#pragma unroll
+                            for (int i = 4 * qa; i < 4 * qa + 4; i++)
+#pragma unroll
+                                for (int j = 4 * qb; j < 4 * qb + 4; j++)
+                                    maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
+                        }
+                    needk |= 1u << k;
+                }
+            }
+            nf += __popc(needk);
+            // Release stage st (mbarrier arrive: release of this warp's reads); the
+            // warp whose arrival completes the phase sees it with a non-blocking
+            // test (acquire) and refills the stage at once — no warp ever blocks
+            // on slower ones (a dedicated producer warp would not fit the register
+            // file).  The CAS hands the refill to exactly one warp.
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&empty[st]);
+                if (gi + STAGES < total && mbar_test(&empty[st], (uint32_t)((gi / STAGES) & 1)) &&
+                    atomicCAS(&claim[st], gi, gi + STAGES) == gi)
+                    issue(gi + STAGES);
             }
         }
+        __syncwarp();
+        exact_flush(p, flist, nf, fmax, I * TB + 1 + TB, iters * KC, s_0, t_0, m, mc, wxp);  // the item's exact pass
+    }
+    if (COUNT && lane == 0) {
+        atomicAdd(p.counters + CTR_SPLITS, (unsigned long long)my_items * iters * KC);
+        atomicAdd(p.counters + CTR_COARSE_PASS, (unsigned long long)c_coarse);
+        atomicAdd(p.counters + CTR_QUADS, (unsigned long long)c_quads);
+        atomicAdd(p.counters + CTR_EXACT, (unsigned long long)c_exact);
     }
 }
 
@@ -707,25 +608,22 @@ bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t pitch,
     return r == CUDA_SUCCESS;
 }
 
-bool make_map32(CUtensorMap *map, const float *base, int64_t rows, int64_t pitch, int box_cols, int box_rows) {
-    auto enc = get_encode();
-    if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)pitch, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)(pitch * 4)};
-    cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-    cuuint32_t estr[2] = {1, 1};
-    static int promo = -1;  // ROTOR_L2PROMO=0|64|128|256 (A/B runs)
-    if (promo < 0) {
-        const char *e = getenv("ROTOR_L2PROMO");
-        promo = e ? atoi(e) : 256;
-    }
-    const CUtensorMapL2promotion pr = promo == 0    ? CU_TENSOR_MAP_L2_PROMOTION_NONE
-                                      : promo == 64  ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
-                                      : promo == 128 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
-                                                     : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
-    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
-                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, pr, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    return r == CUDA_SUCCESS;
+template <int KCW, int STG>
+bool set_wide_attr() {
+    return cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024) != cudaSuccess ||
+           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                227 * 1024) != cudaSuccess;
+}
+
+template <int KCW, int STG>
+void launch_wide(const Problem &p, int delta, int tile_lo, int nt, int coarse, int grid, size_t wx_b, cudaStream_t st) {
+    const int fmax = wide_fmax(p.n, WideRing<KCW, STG>::bytes);
+    const size_t smem = WideRing<KCW, STG>::bytes + wx_b + (size_t)(CONSUMERS / 32) * fmax * 2;
+    if (p.counters)
+        k_tile_middle_wide<KCW, STG, true><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
+    else
+        k_tile_middle_wide<KCW, STG, false><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
 }
 
 }  // namespace tiled
@@ -735,31 +633,38 @@ size_t tiled_extra_bytes(int L, int S) { return tiled::leaf_flag_bytes(L, S); }
 
 int tiled_nb(int n) { return (n + tiled::TB - 1) / tiled::TB; }
 
-// Per-solve setup: kernel attributes, the two tensor maps (over the whole
-// allocations: left pad columns and spare rows included), zeroed leaf flags.
+int64_t tiled_middle_candidates(int n) {
+    using tiled::TB;
+    const int nb = tiled_nb(n);
+    int64_t tot = 0;
+    for (int I = 0; I < nb; I++) {
+        const int cs = min(n, TB * (I + 1)) - TB * I;
+        for (int J = I + 2; J < nb; J++) tot += (int64_t)cs * (min(n, TB * (J + 1)) - TB * J) * (J - I - 1) * TB;
+    }
+    return tot;
+}
+
+// Per-solve setup: kernel attributes, the tensor maps of the exact middle
+// (over the whole allocations: left pad columns and spare rows included),
+// zeroed leaf flags.  The shared-memory opt-in is a per-device function
+// attribute, so it is set on every call (the current device may change
+// between solves; the call is cheap).
 int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     using namespace tiled;
     static_assert(sizeof(CUtensorMap) <= sizeof(ctx->tmA), "tensor map storage");
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_tile_middle<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
-            cudaFuncSetAttribute(k_tile_middle_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(k_tile_middle_wide<WKC, WSTAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 227 * 1024) != cudaSuccess)
-            return -1;
-        attr = true;
-    }
+    if (cudaFuncSetAttribute(k_tile_middle<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
+        set_wide_attr<4, 4>() || set_wide_attr<4, 6>() || set_wide_attr<2, 8>() || set_wide_attr<8, 3>())
+        return -1;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&ctx->sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+        return -1;
     const int n = p.n;
     const int64_t rows = (int64_t)n * (n + 1) / 2;
     if (!make_map(reinterpret_cast<CUtensorMap *>(ctx->tmA), p.A - kPad, rows + kPadRows, p.pitch, TM, TB) ||
         !make_map(reinterpret_cast<CUtensorMap *>(ctx->tmC), p.C - kPad, rows + kPadRows, p.pitch, TMB, TB) ||
-        !p.A32 || !p.C32 ||
-        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmA32), p.A32 - kPad, rows + kPadRows, p.pitch, TM, TB) ||
-        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmC32), p.C32 - kPad, rows + kPadRows, p.pitch, TMB32, TB) ||
-        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmA32w), p.A32 - kPad, rows + kPadRows, p.pitch, TMW, TB) ||
-        !make_map32(reinterpret_cast<CUtensorMap *>(ctx->tmC32w), p.C32 - kPad, rows + kPadRows, p.pitch, TMBW, TB))
+        !p.A32 || !p.C32)
         return -1;
     if (!p.flags || cudaMemsetAsync(p.flags, 0, leaf_flag_bytes(p.L, p.S), st) != cudaSuccess) return -1;
     ctx->phase_id = 0;
@@ -775,48 +680,49 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
     if (tile_hi <= tile_lo) return 0;
     int launches = 0;
     if (delta >= 2) {
-        static int sms = 0;
-        if (!sms) {
-            int dev = 0;
-            cudaGetDevice(&dev);
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        }
-        const int n_items = (tile_hi - tile_lo) * ((p.S + 1 + TM - 1) / TM);
-        const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
-        const size_t smem = SMEM_BYTES + (p.n <= WX_SMEM_MAX ? (size_t)p.n * 4 : 0);
-        const CUtensorMap &tmA = *reinterpret_cast<const CUtensorMap *>(ctx->tmA);
-        const CUtensorMap &tmC = *reinterpret_cast<const CUtensorMap *>(ctx->tmC);
+        const int sms = ctx->sms;
         static int coarse = -1;  // ROTOR_COARSE=0|1 (A/B)
         if (coarse < 0) {
             const char *e = getenv("ROTOR_COARSE");
             coarse = e ? atoi(e) : 1;
         }
-        static int variant = -1;  // ROTOR_MIDDLE=exact|f32|wide (A/B runs; default wide)
+        static int variant = -1;  // ROTOR_MIDDLE=exact|wide (A/B runs; default wide)
         if (variant < 0) {
             const char *e = getenv("ROTOR_MIDDLE");
-            variant = (e && !strcmp(e, "exact")) ? 0 : (e && !strcmp(e, "f32")) ? 1 : 2;
+            variant = (e && !strcmp(e, "exact")) ? 0 : 2;
         }
         const int nt = tile_hi - tile_lo;
         const bool timed = ctx->mid_ev && ctx->mid_n < ctx->mid_cap;
         if (timed) cudaEventRecord(ctx->mid_ev[2 * ctx->mid_n], st);
-        if (variant == 1)
-            k_tile_middle_f32<<<grid, THREADS, F32Ring::bytes + (p.n <= F32_WX_MAX ? (size_t)p.n * 4 : 0), st>>>(
-                *reinterpret_cast<const CUtensorMap *>(ctx->tmA32), *reinterpret_cast<const CUtensorMap *>(ctx->tmC32),
-                p, delta, tile_lo, nt);
-        else if (variant == 2) {
+        if (variant == 2) {
             const int items_w = nt * ((p.S + 1 + TMW - 1) / TMW);
-            // ring geometry (same-box A/B, ms of middle per config-4 solve): KC = 4 x
-            // 6 stages 79.1, x 5 77.3, x 4 76.8, x 3 76.6; KC = 8 x 3 83.5 — the
-            // shallower ring leaves more of the SM's shared-memory/L1 carve-out
-            // to L1 (spill reloads, exact-pass operands)
-            const size_t wx_b = p.n <= WIDE_WX_MAX ? (size_t)p.n * 4 : 0;
-            const CUtensorMap &ma = *reinterpret_cast<const CUtensorMap *>(ctx->tmA32w);
-            const CUtensorMap &mc = *reinterpret_cast<const CUtensorMap *>(ctx->tmC32w);
+            // ring geometry (same-box A/B, ms of middle per config-4 solve, r01 TMA
+            // boxes): KC = 4 x 6 stages 79.1, x 5 77.3, x 4 76.8, x 3 76.6; KC = 8 x 3
+            // 83.5 — the shallower ring leaves more of the SM's shared-memory/L1
+            // carve-out to L1 (spill reloads, exact-pass operands)
+            const size_t wx_b = n_wx_smem(p.n) ? (size_t)p.n * 4 : 0;
             const int gw = items_w < sms ? items_w : sms;
-            k_tile_middle_wide<WKC, WSTAGES><<<gw, THREADS, WideRing<WKC, WSTAGES>::bytes + wx_b, st>>>(
-                ma, mc, p, delta, tile_lo, nt, coarse);
-        } else
-            k_tile_middle<KC, STAGES><<<grid, THREADS, smem, st>>>(tmA, tmC, p, delta, tile_lo, tile_hi - tile_lo);
+            static int ring = -1;  // ROTOR_WRING=44|46|28|83 (KC x stages, A/B runs; default 4 x 4)
+            if (ring < 0) {
+                const char *e = getenv("ROTOR_WRING");
+                ring = e ? atoi(e) : 44;
+            }
+            if (ring == 46)
+                launch_wide<4, 6>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
+            else if (ring == 28)
+                launch_wide<2, 8>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
+            else if (ring == 83)
+                launch_wide<8, 3>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
+            else
+                launch_wide<WKC, WSTAGES>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
+        } else {
+            const int n_items = nt * ((p.S + 1 + TM - 1) / TM);
+            const int grid = n_items < sms ? n_items : sms;  // persistent: one CTA per SM
+            const size_t smem = SMEM_BYTES + (p.n <= WX_SMEM_MAX ? (size_t)p.n * 4 : 0);
+            const CUtensorMap &tmA = *reinterpret_cast<const CUtensorMap *>(ctx->tmA);
+            const CUtensorMap &tmC = *reinterpret_cast<const CUtensorMap *>(ctx->tmC);
+            k_tile_middle<KC, STAGES><<<grid, THREADS, smem, st>>>(tmA, tmC, p, delta, tile_lo, nt);
+        }
         if (timed) cudaEventRecord(ctx->mid_ev[2 * ctx->mid_n++ + 1], st);
         launches++;
     }
@@ -857,18 +763,12 @@ __global__ void k_tile_pack(Problem p, int delta, int tile_lo, double *buf, int 
     double *crow = p.C + cell_index(n, s, t) * p.pitch;
     double *packed = buf + (((int64_t)tile * TB + a) * TB + c) * W;
     const bool has_a = t < n;  // A(s, n) is never an operand
-    double *arow = has_a ? p.A + a_index(s, t) * p.pitch : nullptr;
     const double u = has_a ? __dadd_rn(p.P[t], -p.P[s - 1]) : 0.0;
     for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < W; m += gridDim.x * blockDim.x) {
         if (unpack) {
             const double v = packed[m];
-            crow[m] = v;
-            if (p.C32) p.C32[(crow - p.C) + m] = __double2float_rd(v);
-            if (has_a) {
-                const double av = __dadd_rn(u, v);
-                arow[m] = av;
-                if (p.A32) p.A32[(arow - p.A) + m] = __double2float_rd(av);
-            }
+            store_final_c(p, cell_index(n, s, t), m, p.wx[s - 1], v);
+            if (has_a) store_final_a(p, a_index(s, t), m, __dadd_rn(u, v));
         } else {
             packed[m] = crow[m];
         }

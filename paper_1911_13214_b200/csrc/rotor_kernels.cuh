@@ -40,15 +40,15 @@ size_t tiled_extra_bytes(int L, int S);
 struct TiledCtx {
     alignas(64) unsigned char tmA[128];  // CUtensorMap of the A table
     alignas(64) unsigned char tmC[128];  // CUtensorMap of the C table
-    alignas(64) unsigned char tmA32[128];  // fp32 shadow of A
-    alignas(64) unsigned char tmC32[128];  // fp32 shadow of C
-    alignas(64) unsigned char tmA32w[128];  // the same with the wide middle kernel's boxes
-    alignas(64) unsigned char tmC32w[128];
     int phase_id;                        // leaf launches so far (look-back flag epochs)
     cudaEvent_t *mid_ev;                 // optional (profiling): event pairs around the middle launches
     int mid_cap, mid_n;                  // pairs available / recorded
+    int sms;                             // SM count of the device (set by tiled_prepare)
 };
 int tiled_nb(int n);  // number of TB-stage blocks
+// candidates of the middle ranges per m (cells s in block I, t in block J,
+// splits s' in blocks I+1..J-1, J - I >= 2; existing cells only)
+int64_t tiled_middle_candidates(int n);
 int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st);
 int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int tile_hi, cudaStream_t st);
 size_t tiled_tile_bytes(int S);

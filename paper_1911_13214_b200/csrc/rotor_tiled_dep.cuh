@@ -306,9 +306,9 @@ __device__ __forceinline__ double finish(const Problem &p, int s, int t, int m, 
         const double v = __dadd_rn(p.w[s], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - p.wbx[s])]));
         c = dmin(c, v);
     }
-    store_final_c(p, cell_index(n, s, t) * pitch + m, c);
+    store_final_c(p, cell_index(n, s, t), m, p.wx[s - 1], c);
     const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), c);
-    if (t < n) store_final_a(p, a_index(s, t) * pitch + m, a);
+    if (t < n) store_final_a(p, a_index(s, t), m, a);
     return a;
 }
 
@@ -407,9 +407,9 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
             c1 = best;
         }
         const double cc = dmin(c1, F[c]);
-        store_final_c(p, cell_index(n, s, t) * pitch + m, cc);
+        store_final_c(p, cell_index(n, s, t), m, p.wx[s - 1], cc);
         const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), cc);
-        if (t < n) store_final_a(p, a_index(s, t) * pitch + m, a);
+        if (t < n) store_final_a(p, a_index(s, t), m, a);
         AR[c + 1] = a;
     }
 }
@@ -465,6 +465,7 @@ struct LeafTab {
     int mnull[SB][SB], mall[SB][SB];  // m_null / m_all of cell (s0+r, t0+c); INT_MAX: no cell / gate shut
     int wxl[SB];                      // wxl[j] = wx[s0+j-1]: shift of the left split s' = s0+j
     int wxr[SB];                      // wxr[c] = wx[t0+c-1]: shift of the right split s' = t0+c
+    int wself[SB];                    // wx[s0+r-1]: the C32 pre-shift of row r's cells
     int wbx[SB];                      // wbx[s0+r]: F_all shift of row r
     double w[SB], Ps[SB], Pt[SB];     // w[s0+r], P[s0+r-1], P[t0+c]
     int64_t crow[SB + 1];             // element offset of C cell (s0+j, t0) (columns t0+c follow, pitch apart)
@@ -483,6 +484,7 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
         if (cc == 0) {
             const bool row = ss < n;  // rows s < t <= n
             T.wxl[rr] = rr > 0 && ss <= n ? p.wx[ss - 1] : 0;
+            T.wself[rr] = ss <= n ? p.wx[ss - 1] : 0;
             T.wxr[rr] = t0 + rr <= n ? p.wx[t0 + rr - 1] : 0;
             T.wbx[rr] = row ? p.wbx[ss] : 0;
             T.w[rr] = row ? p.w[ss] : 0.0;
@@ -515,7 +517,7 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     // during the look-back wait: A(s, ·) of the left splits, A(s, t0-1), and
     // the partial minimum of the row's cells
     // addresses from the staged row offsets: cells (s, t0+c) are consecutive rows
-    const double *Cm = p.C + m;
+    double *Cm = p.C + m;
     double AL[SB - 1];  // AL[k] = A(s, s + k): left split s' = s + k + 1 <= ea
 #pragma unroll
     for (int k = 0; k < SB - 1; k++)
@@ -548,6 +550,14 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
         F[c] = m >= T.mall[r][c] ? __dadd_rn(T.w[r], __ldcg(Cm + T.crow[r + 1] + c * pitch - T.wbx[r])) : INFINITY;
     }
     if (RS) cp_async_wait<0>();  // this thread's right-range operands are in shared memory
+    // the row's outputs, addressed incrementally: cells (s, t0+c) are consecutive
+    // C rows (their fp32 shadows consecutive shadow rows, pre-shifted by
+    // wx[s-1]); A(s, t) -> A(s, t+1) is t rows further on (a_index)
+    const int w = T.wself[r];
+    const int64_t c_row = cell_index(n, s, t0);
+    float *c32_hi = (m + w <= p.S) ? p.C32 + shadow_index(p.srows, c_row, m + w) : nullptr;
+    float *c32_lo = (m < w) ? p.C32 + shadow_index(p.srows, c_row, m) : nullptr;
+    int64_t a_row = a_index(s, t0);
 #pragma unroll
     for (int c = 0; c < SB; c++) {
         const int t = t0 + c;
@@ -565,9 +575,15 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
             c1 = best;
         }
         const double cc = dmin(c1, F[c]);
-        store_final_c(p, crow + c * pitch + m, cc);
+        Cm[crow + c * pitch] = cc;  // store_final_c, unrolled
+        if (c32_hi) c32_hi[c * kSW] = __double2float_rd(cc);
+        if (c32_lo) c32_lo[c * kSW] = INFINITY;
         const double a = __dadd_rn(__dadd_rn(T.Pt[c], -T.Ps[r]), cc);
-        if (t < n) store_final_a(p, a_index(s, t) * pitch + m, a);
+        if (t < n) {  // store_final_a
+            p.A[a_row * pitch + m] = a;
+            p.A32[shadow_index(p.srows, a_row, m)] = __double2float_rd(a);
+        }
+        a_row += t;
         AR[c + 1] = a;
     }
 }

@@ -159,7 +159,7 @@ def test_tiled_block_boundaries(R, oracle_mod, L):
 @pytest.mark.parametrize("S", [15, 16, 17, 31, 32, 33, 63, 64, 127, 128, 129, 255, 257, 520])
 def test_tiled_m_chunk_boundaries(R, oracle_mod, S):
     """S + 1 around the m-chunks of the tiled kernels (32 m per wide middle item,
-    16 m per exact/f32 middle item and sub-product warp, 128 m per leaf CTA,
+    16 m per exact middle item and sub-product warp, 128 m per leaf CTA,
     32 / 128 look-back chunks), with
     shifts from a fraction of a chunk to several chunks (big sizes, tight and
     loose limits): full tables bit-exact, both modes."""
@@ -193,19 +193,29 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("variant", ["exact", "f32", "nocoarse"])
-def test_middle_kernel_variants(R, variant):
-    """The non-default middle kernels (read once per process: ROTOR_MIDDLE=exact,
-    the unpruned fp64 k_tile_middle; =f32, the 16-m fp32-filter variant;
-    ROTOR_COARSE=0, the default kernel without its coarse bounds) stay bit-exact
-    against the oracle — run in a subprocess with the variable set."""
+VARIANTS = {
+    "exact": {"ROTOR_MIDDLE": "exact"},  # the unpruned fp64 k_tile_middle
+    "nocoarse": {"ROTOR_COARSE": "0"},  # the pruned middle without its coarse bounds
+    "leaf_row": {"ROTOR_LEAF": "row"},  # k_sub_leaf<false>: scalars from global memory
+    "leaf_tab": {"ROTOR_LEAF": "tab"},  # k_sub_leaf_row<false>: right-range operands not staged
+    "prod4": {"ROTOR_PROD": "1"},  # k_sub_product_async at 4 CTAs/SM
+    "prod_reg3": {"ROTOR_PROD": "3"},  # k_sub_product (operands through registers), 3 CTAs/SM
+    "prod_reg4": {"ROTOR_PROD": "4"},
+}
+
+
+@pytest.mark.parametrize("variant", sorted(VARIANTS))
+def test_kernel_variants(R, variant):
+    """The non-default kernels of the tiled fill (selected once per process by
+    ROTOR_MIDDLE / ROTOR_COARSE / ROTOR_LEAF / ROTOR_PROD, kept for A/B
+    measurements) stay bit-exact against the oracle — run in a subprocess with
+    the variable set."""
     import os
     import subprocess
     import sys
 
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    knob = {"nocoarse": {"ROTOR_COARSE": "0"}}.get(variant, {"ROTOR_MIDDLE": variant})
-    env = dict(os.environ, PYTHONPATH=root, **knob)
+    env = dict(os.environ, PYTHONPATH=root, **VARIANTS[variant])
     r = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT], cwd=root, env=env, capture_output=True, text=True,
                        timeout=600)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
@@ -335,3 +345,65 @@ def test_config4_full_size_sampled(R, oracle_mod, kernel):
 
 def S_top(sz, S):
     return S - sz.wx[0]
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config4_full_table_golden(R, kernel):
+    """Config 4 (L=1000, S=4000, the bench's workload and launch configuration):
+    the WHOLE table against the oracle's full fill, through the checksums of
+    tests/golden/cfg4_L1000_S4000.txt (scripts/make_golden_cfg4.py, oracle only):
+    every row's fp64 bits enter the per-s and per-d checksums, so any differing
+    value fails and is located to its cell (s, s+d).  Also bit-equal: the cost
+    (P:824), the whole top row C[1,L+1,0..S] and Algorithm 2's schedule."""
+    import os
+
+    import table_hash as TH
+
+    g = TH.read_golden(os.path.join(os.path.dirname(__file__), "golden", "cfg4_L1000_S4000.txt"))
+    p = G.config4()
+    ch = p.chain
+    n = ch.L + 1
+    assert (ch.L, p.slots, p.mem_limit) == (int(g["L"]), int(g["S"]), int(g["M"]))
+    res = R.solve(ch, p.mem_limit, p.slots, kernel=kernel)
+    assert res.status == R.OK
+    assert int(bits(np.array([res.cost]))[0]) == int(g["cost"], 16)
+    ops = [(x >> 32, x & 0xFFFFFFFF) for x in g["ops"]]
+    assert res.op_list() == ops
+    top = R.export_rows([(1, n)], p.slots)[0]
+    assert [int(x) for x in bits(top)] == g["top"]
+    hs = TH.TableHasher(n)
+    for s0 in range(1, n + 1, 32):
+        cells = [(s, t) for s in range(s0, min(s0 + 32, n + 1)) for t in range(s, n + 1)]
+        rows = R.export_rows(cells, p.slots)
+        hs.add([c[0] for c in cells], [c[1] for c in cells], TH.row_hashes(rows))
+    assert hs.complete()
+    H = [int(x) for x in hs.H[1:]]
+    Gd = [int(x) for x in hs.G]
+    bad_s = [s + 1 for s in range(n) if H[s] != g["H"][s]]
+    bad_d = [d for d in range(n) if Gd[d] != g["G"][d]]
+    assert not bad_s and not bad_d, f"{kernel}: rows differ from the oracle at s in {bad_s[:10]}, d in {bad_d[:10]}"
+
+
+def test_counters(R, oracle_mod):
+    """options.counters: the pruned middle's work counts are consistent with the
+    geometry (visits = middle warps x splits; every fired split also passed the
+    coarse bound; the middle never compares more than it visits), the nominal
+    count is rotor_transitions, and counting changes no result."""
+    O = oracle_mod
+    p = G.config3()
+    ch = p.chain
+    res0 = R.solve(ch, p.mem_limit, p.slots, kernel="tiled")
+    res = R.solve(ch, p.mem_limit, p.slots, kernel="tiled", counters=True)
+    assert res.cost == res0.cost and res.op_list() == res0.op_list()
+    c = R.last_counters()
+    assert c["nominal"] == R.transitions(ch.L, p.slots)
+    n, TB = ch.L + 1, 32
+    nb = (n + TB - 1) // TB
+    n_mc = (p.slots + 1 + 31) // 32
+    visits = sum((nb - d) * n_mc * 16 * (d - 1) * TB for d in range(2, nb))
+    assert c["middle_split_visits"] == visits
+    assert c["exact_splits"] <= c["coarse_pass"] <= c["middle_split_visits"]
+    assert c["quadrant_compares"] <= 4 * c["coarse_pass"]
+    assert 0 < c["middle_nominal"] < c["nominal"]
+    assert c["evaluated"] == 512.0 * c["quadrant_compares"] + 2048.0 * c["exact_splits"] + c["dependent_nominal"]
+    assert c["evaluated"] < c["nominal"]
