@@ -651,6 +651,8 @@ def run_ours(args):
             "middle_exact_candidates": 2048 * c["exact_splits"],
             "middle_skipped_frac": 1.0 - 512.0 * c["quadrant_compares"] / (2048.0 * c["middle_split_visits"]),
             "dependent_exact": c["dependent_nominal"],
+            "middle_warp_cycles": {k: c[f"middle_{k}_cycles"] for k in ("wait", "init", "loop", "flush")},
+            "middle_warp_imbalance": c["middle_warp_imbalance"],
             "note": "value counts NOMINAL transitions (every cell of diagonal d: d + 1 candidates, Eq. 2); "
                     "evaluated = fp32 filter compares + fp64 exact candidates of the pruned middle + every "
                     "candidate of the dependent phase; the middle skips the rest by exact lower bounds "

@@ -251,6 +251,12 @@ typedef struct {
     uint64_t quadrant_compares;
     uint64_t exact_splits;
     double evaluated;               /* 512 quadrant_compares + 2048 exact_splits + dependent_nominal */
+    /* clock cycles of the middle's warps, summed over warps (where its time goes) */
+    uint64_t middle_wait_cycles;    /* waiting for operand boxes (the bulk-copy ring) */
+    uint64_t middle_init_cycles;    /* item setup (gates, bounds) */
+    uint64_t middle_loop_cycles;    /* the filter over the splits */
+    uint64_t middle_flush_cycles;   /* the exact fp64 pass of the fired splits */
+    double middle_warp_imbalance;   /* max / mean over the 16 warp slots of (loop + flush) cycles */
 } rotor_counters;
 int rotor_last_counters(rotor_counters *out);
 

@@ -64,6 +64,9 @@ class rotor_counters(ctypes.Structure):
         ("nominal", ctypes.c_double), ("middle_nominal", ctypes.c_double), ("dependent_nominal", ctypes.c_double),
         ("middle_split_visits", ctypes.c_uint64), ("coarse_pass", ctypes.c_uint64),
         ("quadrant_compares", ctypes.c_uint64), ("exact_splits", ctypes.c_uint64), ("evaluated", ctypes.c_double),
+        ("middle_wait_cycles", ctypes.c_uint64), ("middle_init_cycles", ctypes.c_uint64),
+        ("middle_loop_cycles", ctypes.c_uint64), ("middle_flush_cycles", ctypes.c_uint64),
+        ("middle_warp_imbalance", ctypes.c_double),
     ]
 
 

@@ -92,7 +92,7 @@ Layout make_layout(int L, int S, const rotor_options &o) {
     y.off_mnull = take((size_t)y.n * y.n * 4);
     y.off_stack = take((size_t)y.stack_cap * sizeof(int4));
     y.off_res = take(64);
-    y.off_ctr = take(64);
+    y.off_ctr = take(256);
     y.off_chain = take(7 * al(n2 * 8));
     y.off_ops = take((size_t)y.ops_cap * sizeof(rotor_op));
     y.off_C = take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 8);
@@ -245,7 +245,7 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
     g_last.stream = st;
     g_last.profiled = o.profile != 0;
     g_last.counted = p.counters != nullptr;
-    if (p.counters) CK(cudaMemsetAsync(p.counters, 0, 64, st));
+    if (p.counters) CK(cudaMemsetAsync(p.counters, 0, 256, st));
     if (o.profile) {
         int r = ensure_events();
         if (r) return r;
@@ -762,7 +762,7 @@ int rotor_last_counters(rotor_counters *out) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     if (dev != g_last.device) CK(cudaSetDevice(g_last.device));
-    unsigned long long c[4];
+    unsigned long long c[8 + 16];
     CK(cudaStreamSynchronize(g_last.stream));
     CK(cudaMemcpy(c, g_last.p.counters, sizeof c, cudaMemcpyDeviceToHost));
     if (dev != g_last.device) CK(cudaSetDevice(dev));
@@ -775,6 +775,16 @@ int rotor_last_counters(rotor_counters *out) {
     out->quadrant_compares = c[2];
     out->exact_splits = c[3];
     out->evaluated = 512.0 * (double)c[2] + 2048.0 * (double)c[3] + out->dependent_nominal;
+    out->middle_wait_cycles = c[4];
+    out->middle_init_cycles = c[5];
+    out->middle_loop_cycles = c[6];
+    out->middle_flush_cycles = c[7];
+    unsigned long long mx = 0, sum = 0;
+    for (int w = 0; w < 16; w++) {
+        mx = std::max(mx, c[8 + w]);
+        sum += c[8 + w];
+    }
+    out->middle_warp_imbalance = sum ? mx * 16.0 / (double)sum : 0.0;
     return ROTOR_OK;
 }
 

@@ -314,12 +314,14 @@ constexpr int FMAX_CAP = 2048;                   // fired splits a warp can reco
 // belongs to exactly one lane, so nothing is atomic.  Rows in pairs keep the
 // running minima in 32 registers.
 __device__ __forceinline__ void exact_flush(const Problem &p, const uint16_t *flist, int nf, int fmax, int sp_lo,
-                                            int n_all, int s_0, int t_0, int m, int mc, const int *wxp) {
-    constexpr int RW = 8, RH = 2;
+                                            int n_all, int s_0, int t_0, int ss, int m, int mc, const int *wxp) {
+    // cells (s_0 + ss*i, t_0 + ss*j), i, j < RW
+    constexpr int RW = 8, RH = 2, FC = 3;  // rows per pass, splits whose loads are in flight together
     const int n = p.n;
     if (m > p.S) return;
     const bool all = nf > fmax;
     const int cnt = all ? n_all : nf;
+    const int64_t sp_pitch = (int64_t)ss * p.pitch;
 #pragma unroll 1
     for (int h = 0; h < RW / RH; h++) {
         double acc[RH][RW];
@@ -328,27 +330,35 @@ __device__ __forceinline__ void exact_flush(const Problem &p, const uint16_t *fl
 #pragma unroll
             for (int j = 0; j < RW; j++) acc[i][j] = INFINITY;
 #pragma unroll 1
-        for (int f = 0; f < cnt; f++) {
-            const int sp = sp_lo + (all ? f : (int)flist[f]);
-            const int mm = mc - wxp[sp - 1];
-            const double *ap = p.A + a_index(s_0 + RH * h, sp - 1) * p.pitch + mc;
-            const double *bp = p.C + cell_index(n, sp, min(t_0, n)) * p.pitch + mm;
-            double ad[RH], bd[RW];
+        for (int f0 = 0; f0 < cnt; f0 += FC) {
+            double ad[FC][RH], bd[FC][RW];
 #pragma unroll
-            for (int i = 0; i < RH; i++) ad[i] = __ldcg(ap + (int64_t)i * p.pitch);
+            for (int u = 0; u < FC; u++) {  // all loads of FC splits first (one memory round trip)
+                const bool live = f0 + u < cnt;
+                const int sp = sp_lo + (live ? (all ? f0 + u : (int)flist[f0 + u]) : 0);
+                const int mm = live ? mc - wxp[sp - 1] : -1;
+                // A(s, sp-1): consecutive s are consecutive rows (a_index); C(sp, t): consecutive t too
+                const double *ap = p.A + a_index(s_0 + ss * RH * h, live ? sp - 1 : s_0) * p.pitch + mc;
+                const double *bp = p.C + cell_index(n, live ? sp : s_0, min(t_0, n)) * p.pitch + mm;
 #pragma unroll
-            for (int j = 0; j < RW; j++) bd[j] = (mm >= 0 && t_0 + j <= n) ? __ldcg(bp + (int64_t)j * p.pitch) : INFINITY;
+                for (int i = 0; i < RH; i++) ad[u][i] = live ? __ldcg(ap + i * sp_pitch) : INFINITY;
 #pragma unroll
-            for (int i = 0; i < RH; i++)
+                for (int j = 0; j < RW; j++)
+                    bd[u][j] = (mm >= 0 && t_0 + ss * j <= n) ? __ldcg(bp + j * sp_pitch) : INFINITY;
+            }
 #pragma unroll
-                for (int j = 0; j < RW; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(ad[i], bd[j]));
+            for (int u = 0; u < FC; u++)
+#pragma unroll
+                for (int i = 0; i < RH; i++)
+#pragma unroll
+                    for (int j = 0; j < RW; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(ad[u][i], bd[u][j]));
         }
 #pragma unroll
         for (int i = 0; i < RH; i++) {
-            double *crow = p.C + cell_index(n, s_0 + RH * h + i, min(t_0, n)) * p.pitch + m;
+            double *crow = p.C + cell_index(n, s_0 + ss * (RH * h + i), min(t_0, n)) * p.pitch + m;
 #pragma unroll
             for (int j = 0; j < RW; j++)
-                if (t_0 + j <= n) crow[(int64_t)j * p.pitch] = acc[i][j];
+                if (t_0 + ss * j <= n) crow[j * sp_pitch] = acc[i][j];
         }
     }
 }
@@ -382,9 +392,12 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 }
 
 // profile counters (Problem::counters, rotor_counters order)
-enum { CTR_SPLITS = 0, CTR_COARSE_PASS = 1, CTR_QUADS = 2, CTR_EXACT = 3, CTR_N = 4 };
+// (COUNT also sums per-warp clock cycles: waiting for stage data, item setup
+// (bestf init), filter loop, exact pass)
+enum { CTR_SPLITS = 0, CTR_COARSE_PASS = 1, CTR_QUADS = 2, CTR_EXACT = 3, CTR_WAIT = 4, CTR_INIT = 5, CTR_LOOP = 6,
+       CTR_FLUSH = 7, CTR_N = 8 };
 
-template <int KCW, int STG, bool COUNT>
+template <int KCW, int STG, bool COUNT, int SS>
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle_wide(Problem p, int delta, int tile_lo, int n_tiles, int coarse, int fmax) {
     using R = WideRing<KCW, STG>;
@@ -446,12 +459,22 @@ __global__ void __launch_bounds__(THREADS, 1)
     __syncwarp();
 
     unsigned c_coarse = 0, c_quads = 0, c_exact = 0;  // profile counters (warp-uniform, COUNT only)
+    unsigned long long c_wait = 0, c_init = 0, c_loop = 0, c_flush = 0, t_mark = COUNT ? clock64() : 0;
+    auto lap = [&](unsigned long long &acc) {
+        if (COUNT) {
+            const unsigned long long t = clock64();
+            acc += t - t_mark;
+            t_mark = t;
+        }
+    };
     const int sg = warp / (TB / RW), tg = warp % (TB / RW);
     uint16_t *flist = fl_s + warp * fmax;  // this warp's fired splits of the current item (s' - sp_lo)
     for (int kl = 0; kl < my_items; kl++) {
         const int item = (int)blockIdx.x + kl * (int)gridDim.x;
         const int I = tile_lo + item / n_mc, J = I + delta;
-        const int s_0 = I * TB + 1 + sg * RW, t_0 = J * TB + 1 + tg * RW;
+        // the warp's 8 x 8 cells (s_0 + SS*i, t_0 + SS*j): SS = 1 a contiguous
+        // sub-tile, SS = 4 spread over the whole tile (balances the warps' work)
+        const int s_0 = I * TB + 1 + sg * (SS == 1 ? RW : 1), t_0 = J * TB + 1 + tg * (SS == 1 ? RW : 1);
         const int m = (item % n_mc) * TMW + lane;
         const int mc = min(m, p.S);
         // bestf >= the exact partial minimum; -inf on cells whose partial is
@@ -461,8 +484,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < RW; i++)
 #pragma unroll
             for (int j = 0; j < RW; j++) {
-                const int t = t_0 + j;
-                bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + i, t)) ? INFINITY : -INFINITY;
+                const int t = t_0 + SS * j;
+                bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + SS * i, t)) ? INFINITY : -INFINITY;
             }
         float maxq[2][2];  // >= every bestf of the lane's 4 x 4 quadrants
 #pragma unroll
@@ -476,20 +499,23 @@ __global__ void __launch_bounds__(THREADS, 1)
                     for (int j = 4 * qb; j < 4 * qb + 4; j++) maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
             }
         int nf = 0;  // fired splits of this item (warp-uniform; > fmax: the list overflowed)
+        lap(c_init);
         for (int it = 0; it < iters; it++) {
             const int gi = kl * iters + it;
             const int st = gi % STAGES;
+            lap(c_loop);
             mbar_wait(&full[st], (uint32_t)((gi / STAGES) & 1));
-            const float *a_f = ring + st * ST + (sg * RW) * TMW + lane;
-            const float *b_f = ring + st * ST + KC * BOX + (tg * RW) * TMW + lane;
+            lap(c_wait);
+            const float *a_f = ring + st * ST + (s_0 - I * TB - 1) * TMW + lane;
+            const float *b_f = ring + st * ST + KC * BOX + (t_0 - J * TB - 1) * TMW + lane;
             unsigned needk = 0;
 #pragma unroll 1
             for (int k = 0; k < KC; k++) {
                 float a[RW], b[RW];
 #pragma unroll
-                for (int i = 0; i < RW; i++) a[i] = a_f[k * BOX + i * TMW];
+                for (int i = 0; i < RW; i++) a[i] = a_f[k * BOX + SS * i * TMW];
 #pragma unroll
-                for (int j = 0; j < RW; j++) b[j] = b_f[k * BOX + j * TMW];
+                for (int j = 0; j < RW; j++) b[j] = b_f[k * BOX + SS * j * TMW];
                 // coarse bounds first: per 4 x 4 quadrant (qa, qb) of the lane's
                 // tile, fadd_rd(min a over its rows, min b over its columns) is
                 // <= every lb of the quadrant (monotone rounding) and maxq >= every
@@ -568,13 +594,21 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
         }
         __syncwarp();
-        exact_flush(p, flist, nf, fmax, I * TB + 1 + TB, iters * KC, s_0, t_0, m, mc, wxp);  // the item's exact pass
+        lap(c_loop);
+        exact_flush(p, flist, nf, fmax, I * TB + 1 + TB, iters * KC, s_0, t_0, SS, m, mc, wxp);  // the item's exact pass
+        __syncwarp();
+        lap(c_flush);
     }
     if (COUNT && lane == 0) {
         atomicAdd(p.counters + CTR_SPLITS, (unsigned long long)my_items * iters * KC);
         atomicAdd(p.counters + CTR_COARSE_PASS, (unsigned long long)c_coarse);
         atomicAdd(p.counters + CTR_QUADS, (unsigned long long)c_quads);
         atomicAdd(p.counters + CTR_EXACT, (unsigned long long)c_exact);
+        atomicAdd(p.counters + CTR_WAIT, c_wait);
+        atomicAdd(p.counters + CTR_INIT, c_init);
+        atomicAdd(p.counters + CTR_LOOP, c_loop);
+        atomicAdd(p.counters + CTR_FLUSH, c_flush);
+        atomicAdd(p.counters + CTR_N + warp, c_loop + c_flush);  // per warp slot (balance across warps)
     }
 }
 
@@ -610,20 +644,34 @@ bool make_map(CUtensorMap *map, const double *base, int64_t rows, int64_t pitch,
 
 template <int KCW, int STG>
 bool set_wide_attr() {
-    return cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024) != cudaSuccess ||
-           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                227 * 1024) != cudaSuccess;
+    const int b = 227 * 1024;
+    const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    return cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, false, 1>, a, b) != cudaSuccess ||
+           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, true, 1>, a, b) != cudaSuccess ||
+           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, false, 4>, a, b) != cudaSuccess ||
+           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, true, 4>, a, b) != cudaSuccess;
 }
 
 template <int KCW, int STG>
 void launch_wide(const Problem &p, int delta, int tile_lo, int nt, int coarse, int grid, size_t wx_b, cudaStream_t st) {
     const int fmax = wide_fmax(p.n, WideRing<KCW, STG>::bytes);
     const size_t smem = WideRing<KCW, STG>::bytes + wx_b + (size_t)(CONSUMERS / 32) * fmax * 2;
-    if (p.counters)
-        k_tile_middle_wide<KCW, STG, true><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
-    else
-        k_tile_middle_wide<KCW, STG, false><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
+    static int ss = -1;  // ROTOR_WSPREAD=1: warps' cells spread over the tile (A/B)
+    if (ss < 0) {
+        const char *e = getenv("ROTOR_WSPREAD");
+        ss = (e && atoi(e)) ? 4 : 1;
+    }
+    if (ss == 4) {
+        if (p.counters)
+            k_tile_middle_wide<KCW, STG, true, 4><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
+        else
+            k_tile_middle_wide<KCW, STG, false, 4><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
+    } else {
+        if (p.counters)
+            k_tile_middle_wide<KCW, STG, true, 1><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
+        else
+            k_tile_middle_wide<KCW, STG, false, 1><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
+    }
 }
 
 }  // namespace tiled

@@ -19,7 +19,8 @@ try:
     d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
     r = d["roofline"]; w = d.get("work") or {}
     print(sys.argv[2] or "default", "solve %.2f ms  fill %.2f  middle %.2f  frac %.3f" % (d["ms_per_step"], d["fill_ms"], r.get("middle_ms_per_step", 0), r["frac"]),
-          " coarse_pass/visits %.3f quads %.3g exact %.3g" % (w.get("middle_coarse_bound_evals", 0) / 32 / max(1, w.get("middle_split_visits", 1)) - 1, w.get("middle_filter_compares", 0), w.get("middle_exact_candidates", 0)) if w else "")
+          " coarse_pass/visits %.3f quads %.3g exact %.3g" % ((w.get("middle_coarse_bound_evals", 0) / 32 / max(1, w.get("middle_split_visits", 1)) - 1) / 4, w.get("middle_filter_compares", 0), w.get("middle_exact_candidates", 0)) if w else "",
+          " cycles " + " ".join("%s %.2f" % (k, v / max(1, sum(w["middle_warp_cycles"].values()))) for k, v in w["middle_warp_cycles"].items()) + " imbalance %.3f" % w.get("middle_warp_imbalance", 0) if w.get("middle_warp_cycles") else "")
 except Exception as e:
     print(sys.argv[2], "bench failed", e, open(sys.argv[1].replace(".json", ".err")).read()[-800:])
 PY
