@@ -131,24 +131,69 @@ int64_t rotor_max_ops(int32_t L);
 /* ---------------------------------------------------------------------------
  * Batched multi-limit solve ("Algorithm 1 for 10 different memory
  * limits"): n_chains chains x n_limits limits, each pair its own table with
- * slot size limits[i*n_limits+j]/S (§5.2).  Runs on the current device.
+ * slot size limits[i*n_limits+j]/S (§5.2).  SURVEY.md §8(e) 1: the problems
+ * are independent, so they are spread over a device list with no exchange.
  *   chains[i], Ls[i]          : host chains
  *   limits[i*n_limits + j]    : bytes
+ *   devices, n_devices        : where to run.  devices == NULL && n_devices == 0:
+ *                               the current device, on `stream`.  A list of
+ *                               n_devices >= 1 CUDA ordinals (an ordinal may
+ *                               repeat): the problems are split by LPT on their
+ *                               nominal transitions (rotor_partition_lpt), one
+ *                               host thread per entry, each with its own stream
+ *                               and library workspace on its device; `stream`
+ *                               is then unused.  devices == NULL && n_devices < 0:
+ *                               every visible device.
  *   costs[i*n_limits + j]     : out
  *   ops + ops_offsets[p]      : out, problem p = i*n_limits + j writes at most ops_caps[p]
  *                               ops at ops + ops_offsets[p] (ops may be NULL: costs only)
  *   n_ops[p]                  : out (-1 if infeasible); may be NULL
- *   status[p]                 : out rotor_status per problem; may be NULL
- * Returns ROTOR_OK if every problem ran (individual infeasibility is reported
- * in status[]), else the first error.
+ *   status[p]                 : out rotor_status per problem (OK, INFEASIBLE,
+ *                               ETRUNC when ops[] was too short); may be NULL
+ * Blocks until every result is on the host.  Returns ROTOR_OK if every
+ * problem ran (individual infeasibility is reported in status[]), else the
+ * first error (with the failing device in rotor_last_error()).
  * ------------------------------------------------------------------------- */
 int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_chains, const uint64_t *limits,
-                      int32_t n_limits, int32_t slots, const rotor_options *opt, void *stream, double *costs,
-                      rotor_op *ops, const int64_t *ops_offsets, const int64_t *ops_caps, int64_t *n_ops,
-                      int32_t *status);
+                      int32_t n_limits, int32_t slots, const rotor_options *opt, const int32_t *devices,
+                      int32_t n_devices, void *stream, double *costs, rotor_op *ops, const int64_t *ops_offsets,
+                      const int64_t *ops_caps, int64_t *n_ops, int32_t *status);
 
 /* ---------------------------------------------------------------------------
- * Sharded single-table solve, for one process per GPU.
+ * One table sharded over a device list, driven from ONE process (SURVEY.md
+ * §8(e) 2).  The tiled fill's 32 x 32-stage tiles of tile diagonal delta
+ * depend only on tiles of smaller delta (Theorem 1 reads strictly shorter
+ * intervals), so per delta every device computes a contiguous,
+ * balanced range of the tiles, and the finished tiles travel to the others
+ * before delta + 1:
+ *   halo_mode 0: the owner packs its tiles' C rows into a staging buffer, each
+ *                other device pulls the buffer with a peer copy
+ *                (cudaMemcpyPeerAsync over NVLink) and unpacks it;
+ *   halo_mode 1: fused peer pull — each other device's unpack kernel reads the
+ *                owner's C rows directly through peer memory (P2P loads over
+ *                NVLink), no staging buffer (needs peer access; falls back to
+ *                mode 0 where a pair has none).
+ * Receivers rebuild the A rows and the fp32 shadows from C with the fill's own
+ * association (Q12), so results are bit-identical to rotor_solve.  Devices
+ * synchronise by CUDA events only; the host thread only enqueues.  The first
+ * device runs Algorithm 2 on its complete table.
+ *   chain, L, mem_limit, slots, opt : as rotor_solve_ex (host chain; the fill is the tiled one)
+ *   devices, n_devices : CUDA ordinals (an ordinal may repeat: several shards on
+ *                        one device, each with its own workspace); devices ==
+ *                        NULL: ordinals 0..n_devices-1 (n_devices < 0: every
+ *                        visible device)
+ *   cost_out, ops, ops_cap, n_ops_out : as rotor_solve
+ * Library workspaces (one per entry, rotor_workspace_bytes each) are leased
+ * for the call; the first entry's table is this thread's "last solve"
+ * (rotor_export_*).  Blocks until the result is on the host.
+ * ------------------------------------------------------------------------- */
+int rotor_solve_sharded(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int32_t slots,
+                        const rotor_options *opt, const int32_t *devices, int32_t n_devices, int32_t halo_mode,
+                        double *cost_out, rotor_op *ops, int64_t ops_cap, int64_t *n_ops_out);
+
+/* ---------------------------------------------------------------------------
+ * Sharded single-table solve, for one process per GPU
+ * (the building blocks rotor_solve_sharded drives itself in one process).
  * The tiled fill cuts the (s,t) triangle into 32x32-stage tiles processed by
  * tile diagonal delta = 0 .. rotor_tile_blocks(L)-1; every tile of one delta
  * depends only on tiles of smaller delta (Theorem 1 reads strictly shorter

@@ -83,8 +83,10 @@ _lib.rotor_solve_device.argtypes = [_P(rotor_chain), _i32, _u64, _i32, _P(rotor_
 _lib.rotor_workspace_bytes.argtypes = [_i32, _i32, _P(rotor_options), _P(_u64)]
 _lib.rotor_max_ops.argtypes = [_i32]
 _lib.rotor_max_ops.restype = _i64
-_lib.rotor_solve_batch.argtypes = [_P(rotor_chain), _P(_i32), _i32, _P(_u64), _i32, _i32, _P(rotor_options), _vp,
-                                   _P(_d), _vp, _P(_i64), _P(_i64), _P(_i64), _P(_i32)]
+_lib.rotor_solve_batch.argtypes = [_P(rotor_chain), _P(_i32), _i32, _P(_u64), _i32, _i32, _P(rotor_options), _P(_i32),
+                                   _i32, _vp, _P(_d), _vp, _P(_i64), _P(_i64), _P(_i64), _P(_i32)]
+_lib.rotor_solve_sharded.argtypes = [_P(rotor_chain), _i32, _u64, _i32, _P(rotor_options), _P(_i32), _i32, _i32,
+                                     _P(_d), _vp, _i64, _P(_i64)]
 _lib.rotor_partition_lpt.argtypes = [_P(_d), _i32, _i32, _P(_i32)]
 _lib.rotor_transitions.argtypes = [_i32, _i32]
 _lib.rotor_transitions.restype = _d
@@ -108,7 +110,7 @@ _lib.rotor_version.restype = _i32
 # every symbol include/rotor.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "rotor_solve", "rotor_solve_ex", "rotor_solve_device", "rotor_workspace_bytes", "rotor_max_ops",
-    "rotor_solve_batch", "rotor_partition_lpt", "rotor_transitions", "rotor_export_tables", "rotor_export_rows",
+    "rotor_solve_batch", "rotor_solve_sharded", "rotor_partition_lpt", "rotor_transitions", "rotor_export_tables", "rotor_export_rows",
     "rotor_last_timings", "rotor_last_counters",
     "rotor_release", "rotor_last_error", "rotor_version",
     "rotor_tile_blocks", "rotor_tile_bytes", "rotor_sharded_begin", "rotor_sharded_step", "rotor_sharded_pack",
@@ -277,9 +279,21 @@ def last_counters() -> dict:
     return {k: getattr(c, k) for k, _ in rotor_counters._fields_}
 
 
-def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=None, **opts):
-    """rotor_solve_batch: len(chains) x len(limits[i]) independent solves on the current device.
+def _devices(devices):
+    """None -> (NULL, 0): the current device; "all" -> (NULL, -1); a list -> (int32 array, len)."""
+    if devices is None:
+        return None, 0
+    if isinstance(devices, str) and devices == "all":
+        return None, -1
+    d = np.ascontiguousarray(list(devices), dtype=np.int32)
+    return d, len(d)
 
+
+def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=None, devices=None, **opts):
+    """rotor_solve_batch: len(chains) x len(limits[i]) independent solves.
+
+    devices: None (the current device, on `stream`), "all", or a list of CUDA
+    ordinals (repeats allowed) the problems are LPT-split over.
     Returns (costs [n_chains, n_limits], status, n_ops, ops list-of-arrays or None).
     """
     nc = len(chains)
@@ -298,9 +312,10 @@ def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=No
         offs = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.int64)
         ops = np.zeros((int(caps.sum()), 2), dtype=np.int32)
     P = lambda a, t: a.ctypes.data_as(_P(t)) if a is not None else None
-    r = _lib.rotor_solve_batch(arr, P(Ls, _i32), nc, P(lim, _u64), nl, int(slots), _c.byref(o), _stream_ptr(stream),
-                               P(costs, _d), ops.ctypes.data if ops is not None else None, P(offs, _i64),
-                               P(caps, _i64), P(n_ops, _i64), P(status, _i32))
+    dv, nd = _devices(devices)
+    r = _lib.rotor_solve_batch(arr, P(Ls, _i32), nc, P(lim, _u64), nl, int(slots), _c.byref(o), P(dv, _i32), nd,
+                               _stream_ptr(stream), P(costs, _d), ops.ctypes.data if ops is not None else None,
+                               P(offs, _i64), P(caps, _i64), P(n_ops, _i64), P(status, _i32))
     _check(r)
     out_ops = None
     if with_ops:
@@ -309,6 +324,32 @@ def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=No
             k = int(n_ops.reshape(-1)[p])
             out_ops.append(ops[offs[p]: offs[p] + max(k, 0)].copy())
     return costs, status, n_ops, out_ops
+
+
+def solve_sharded(chain, mem_limit: int, slots: int, devices, *, halo_mode: int = 1, ops_cap: int | None = None,
+                  **opts) -> Result:
+    """rotor_solve_sharded: ONE table sharded over `devices` (list of CUDA ordinals,
+    repeats allowed; "all"; or an int k: ordinals 0..k-1) from this process,
+    tiles exchanged per tile diagonal by peer pull (halo_mode 1) or pack + peer
+    copy (halo_mode 0).  Bit-identical to solve()."""
+    c, keep = _host_chain(chain)
+    L = int(chain.L)
+    if isinstance(devices, int):
+        dv, nd = None, int(devices)
+    else:
+        dv, nd = _devices(devices)
+    cap = max_ops(L) if ops_cap is None else int(ops_cap)
+    ops = np.zeros((max(cap, 1), 2), dtype=np.int32)
+    cost = _d()
+    n_ops = _i64(0)
+    o = _options(**opts)
+    r = _lib.rotor_solve_sharded(_c.byref(c), L, int(mem_limit), int(slots), _c.byref(o),
+                                 dv.ctypes.data_as(_P(_i32)) if dv is not None else None, nd, int(halo_mode),
+                                 _c.byref(cost), ops.ctypes.data if cap > 0 else None, cap, _c.byref(n_ops))
+    _check(r, allow=(OK, INFEASIBLE, ETRUNC))
+    del keep
+    k = int(n_ops.value) if r != INFEASIBLE else 0
+    return Result(r, float(cost.value), ops[: min(k, cap)].copy(), k)
 
 
 def partition_lpt(weights, n_parts: int) -> np.ndarray:

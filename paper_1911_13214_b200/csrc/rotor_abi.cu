@@ -7,7 +7,9 @@
 #include <string.h>
 
 #include <algorithm>
+#include <atomic>
 #include <map>
+#include <thread>
 #include <mutex>
 #include <numeric>
 #include <vector>
@@ -167,6 +169,61 @@ int check_host_chain(const rotor_chain *c, int L) {
     return ROTOR_OK;
 }
 
+// ---- library-owned cached workspaces ----
+// One entry per (device, kind): kind 0 = rotor_solve / rotor_solve_ex, kind
+// kBatchKind + w = batch worker w, kShardKind + r = sharded rank r.  A call
+// LEASES its entry for its whole duration (the entry's mutex), so two threads
+// never share a workspace; a call that grows an entry frees the old buffer.
+// `gen` counts the solves an entry has served: the last-solve record keeps it,
+// and the export calls refuse to read an entry a later call has reused.
+constexpr int kBatchKind = 16, kShardKind = 4096;
+struct CacheEntry {
+    std::mutex mu;
+    void *ptr = nullptr;
+    size_t bytes = 0;
+    std::atomic<uint64_t> gen{0};
+};
+std::mutex g_cache_mu;
+std::map<std::pair<int, int>, std::unique_ptr<CacheEntry>> g_cache;
+
+struct Lease {
+    CacheEntry *e = nullptr;
+    std::unique_lock<std::mutex> lk;
+};
+
+int lease_workspace(int kind, size_t bytes, Lease &l, void **out) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CacheEntry *e;
+    {
+        std::lock_guard<std::mutex> g(g_cache_mu);
+        auto &slot = g_cache[{dev, kind}];
+        if (!slot) slot.reset(new CacheEntry());
+        e = slot.get();
+    }
+    l.lk = std::unique_lock<std::mutex>(e->mu);
+    l.e = e;
+    if (e->bytes < bytes) {
+        if (e->ptr) {
+            cudaDeviceSynchronize();
+            cudaFree(e->ptr);
+            e->ptr = nullptr;
+            e->bytes = 0;
+        }
+        void *p = nullptr;
+        cudaError_t err = cudaMalloc(&p, bytes);
+        if (err != cudaSuccess) {
+            cudaGetLastError();
+            return fail(ROTOR_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(err));
+        }
+        e->ptr = p;
+        e->bytes = bytes;
+    }
+    e->gen++;
+    *out = e->ptr;
+    return ROTOR_OK;
+}
+
 // ---- per-thread record of the last solve (export / timings) ----
 struct LastSolve {
     bool valid = false;
@@ -180,39 +237,23 @@ struct LastSolve {
     std::vector<cudaEvent_t> mid_ev;  // pairs around the tiled fill's middle launches
     int mid_n = 0;
     bool counted = false;  // options.counters: p.counters holds this solve's middle counters
+    CacheEntry *cache = nullptr;  // the library workspace the tables live in (nullptr: caller-owned)
+    uint64_t cache_gen = 0;
 };
 thread_local LastSolve g_last;
+
+// The tables of the last solve are still readable: a library workspace may
+// have been reused by a later call (of any thread) since.
+int check_last_alive() {
+    if (!g_last.valid) return fail(ROTOR_EINPUT, "no solve on this thread");
+    if (g_last.cache && g_last.cache->gen.load() != g_last.cache_gen)
+        return fail(ROTOR_EINVALID, "the library workspace of the last solve was reused by a later call");
+    return ROTOR_OK;
+}
 
 int ensure_events() {
     for (auto &e : g_last.ev)
         if (!e) CK(cudaEventCreate(&e));
-    return ROTOR_OK;
-}
-
-// ---- library-owned cached workspaces (per device) ----
-std::mutex g_cache_mu;
-std::map<int, std::pair<void *, size_t>> g_cache;
-
-int cached_workspace(size_t bytes, void **out) {
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    std::lock_guard<std::mutex> lk(g_cache_mu);
-    auto &e = g_cache[dev];
-    if (e.second < bytes) {
-        if (e.first) {
-            cudaDeviceSynchronize();
-            cudaFree(e.first);
-            e = {nullptr, 0};
-        }
-        void *p = nullptr;
-        cudaError_t err = cudaMalloc(&p, bytes);
-        if (err != cudaSuccess) {
-            cudaGetLastError();
-            return fail(ROTOR_ENOMEM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(err));
-        }
-        e = {p, bytes};
-    }
-    *out = e.first;
     return ROTOR_OK;
 }
 
@@ -245,6 +286,7 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
     g_last.stream = st;
     g_last.profiled = o.profile != 0;
     g_last.counted = p.counters != nullptr;
+    g_last.cache = nullptr;
     if (p.counters) CK(cudaMemsetAsync(p.counters, 0, 256, st));
     if (o.profile) {
         int r = ensure_events();
@@ -287,6 +329,159 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
     if (o.profile) CK(cudaEventRecord(g_last.ev[3], st));
     g_last.fill_launches = fill;
     g_last.total_launches = launches;
+    return ROTOR_OK;
+}
+
+// ---- batched independent solves (rotor_solve_batch) ----
+struct BatchIn {
+    const rotor_chain *chains;
+    const int32_t *Ls;
+    int32_t n_chains;
+    const uint64_t *limits;
+    int32_t n_limits, slots;
+    rotor_options o;
+    rotor_op *ops;
+    const int64_t *ops_offsets, *ops_caps;
+};
+struct BatchOut {
+    double *costs;
+    int64_t *n_ops;
+    int32_t *status;
+};
+
+// The problems idx (global index q = chain * n_limits + limit) on the current
+// device: one fused k_batch launch on `st`, results scattered to the caller's
+// arrays at their global indices (distinct workers write disjoint entries).
+int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind, cudaStream_t st,
+                    const BatchOut &out) {
+    const int64_t P = (int64_t)idx.size();
+    if (P == 0) return ROTOR_OK;
+    const int n_chains = in.n_chains, slots = in.slots;
+    int dev = 0, sms = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int L_max = 0;
+    for (int i = 0; i < n_chains; i++) L_max = std::max(L_max, (int)in.Ls[i]);
+
+    // host staging: chains padded to a common stride, problem descriptors
+    const int64_t stride = L_max + 2;
+    std::vector<double> h_d(2 * n_chains * stride, 0.0);
+    std::vector<uint64_t> h_u(5 * n_chains * stride, 0);
+    for (int i = 0; i < n_chains; i++) {
+        const int n1 = in.Ls[i] + 1;
+        memcpy(&h_d[(0 * n_chains + i) * stride], in.chains[i].uf, n1 * 8);
+        memcpy(&h_d[(1 * n_chains + i) * stride], in.chains[i].ub, n1 * 8);
+        memcpy(&h_u[(0 * n_chains + i) * stride], in.chains[i].wx, n1 * 8);
+        memcpy(&h_u[(1 * n_chains + i) * stride], in.chains[i].wbx, n1 * 8);
+        memcpy(&h_u[(2 * n_chains + i) * stride], in.chains[i].wy, (n1 + 1) * 8);
+        memcpy(&h_u[(3 * n_chains + i) * stride], in.chains[i].of, n1 * 8);
+        memcpy(&h_u[(4 * n_chains + i) * stride], in.chains[i].ob, n1 * 8);
+    }
+    std::vector<int32_t> h_pc(P), h_L(in.Ls, in.Ls + n_chains);
+    std::vector<uint64_t> h_lim(P);
+    std::vector<int64_t> h_off(P, 0), h_cap(P, 0);
+    int64_t total_ops = 0;
+    for (int64_t k = 0; k < P; k++) {
+        const int64_t q = idx[k];
+        h_pc[k] = (int32_t)(q / in.n_limits);
+        h_lim[k] = in.limits[q];
+        if (in.ops) {
+            h_cap[k] = std::max<int64_t>(0, in.ops_caps[q]);
+            h_off[k] = total_ops;
+            total_ops += h_cap[k];
+        }
+    }
+    // queue order: the longest chains first (cost ~ L^3 at a common S): the
+    // short tables fill the tail instead of a long one starting last
+    std::vector<int32_t> h_order(P);
+    for (int64_t k = 0; k < P; k++) h_order[k] = (int32_t)k;
+    std::stable_sort(h_order.begin(), h_order.end(),
+                     [&](int32_t x, int32_t y) { return in.Ls[h_pc[x]] > in.Ls[h_pc[y]]; });
+    // persistent k_batch CTAs (512 threads, 32 registers): four resident per SM,
+    // a full SM of threads (config 5: 1 per SM 86.4 ms, 2 59.0, 3 50.0 at 40
+    // registers / 47.5 at 32, 4 44.6; 256 threads x 6 62.6, x 7 60.6; 384 x 4
+    // 50.6; 128 x 12 91.2)
+    const int n_slots = (int)std::min<int64_t>(P, 4 * (int64_t)sms);
+    const size_t slot = rotor::batch_slot_bytes(L_max, slots);
+    // one device allocation (a leased library workspace): descriptors, outputs, ops, then the slot pool
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t r = off;
+        off += al(bytes);
+        return r;
+    };
+    const size_t o_d = take(h_d.size() * 8), o_u = take(h_u.size() * 8), o_pc = take(P * 4), o_L = take(n_chains * 4),
+                 o_lim = take(P * 8), o_off = take(P * 8), o_cap = take(P * 8), o_cost = take(P * 8),
+                 o_nops = take(P * 8), o_st = take(P * 4), o_ops = take((size_t)std::max<int64_t>(total_ops, 1) * 8),
+                 o_ctr = take(8), o_ord = take(P * 4), o_pool = take((size_t)n_slots * slot);
+    void *wsv = nullptr;
+    Lease lease;
+    int r = lease_workspace(kind, off, lease, &wsv);
+    if (r) return r;
+    char *w = (char *)wsv;
+    CK(cudaMemcpyAsync(w + o_d, h_d.data(), h_d.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_u, h_u.data(), h_u.size() * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_pc, h_pc.data(), P * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_L, h_L.data(), n_chains * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_lim, h_lim.data(), P * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_off, h_off.data(), P * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_cap, h_cap.data(), P * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(w + o_ord, h_order.data(), P * 4, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(w + o_ctr, 0, 8, st));
+    rotor::BatchArgs b{};
+    b.n_problems = (int)P;
+    b.S = slots;
+    b.restricted = in.o.restricted ? 1 : 0;
+    b.L_max = L_max;
+    b.prob_chain = (const int32_t *)(w + o_pc);
+    b.limits = (const uint64_t *)(w + o_lim);
+    b.chain_L = (const int32_t *)(w + o_L);
+    b.chain_stride = stride;
+    b.uf = (const double *)(w + o_d);
+    b.ub = (const double *)(w + o_d) + n_chains * stride;
+    b.wx = (const uint64_t *)(w + o_u);
+    b.wbx = (const uint64_t *)(w + o_u) + 1 * n_chains * stride;
+    b.wy = (const uint64_t *)(w + o_u) + 2 * n_chains * stride;
+    b.of = (const uint64_t *)(w + o_u) + 3 * n_chains * stride;
+    b.ob = (const uint64_t *)(w + o_u) + 4 * n_chains * stride;
+    b.pool = w + o_pool;
+    b.cost = (double *)(w + o_cost);
+    b.nops = (int64_t *)(w + o_nops);
+    b.status = (int32_t *)(w + o_st);
+    b.ops = in.ops ? (rotor_op *)(w + o_ops) : nullptr;
+    b.ops_off = (const int64_t *)(w + o_off);
+    b.ops_cap = (const int64_t *)(w + o_cap);
+    b.counter = (int *)(w + o_ctr);
+    b.order = (const int32_t *)(w + o_ord);
+    rotor::launch_batch(b, n_slots, st);
+    CK(cudaGetLastError());
+    std::vector<double> h_c(P);
+    std::vector<int64_t> h_n(P);
+    std::vector<int32_t> h_s(P);
+    CK(cudaMemcpyAsync(h_c.data(), w + o_cost, P * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_n.data(), w + o_nops, P * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_s.data(), w + o_st, P * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    int first_err = ROTOR_OK;
+    for (int64_t k = 0; k < P; k++) {
+        const int64_t q = idx[k];
+        int sq = h_s[k];
+        // costs-only mode (ops == NULL): the device reports ETRUNC for every
+        // feasible problem (no op buffer) — that is a plain success here
+        if (sq == ROTOR_ETRUNC && !in.ops) sq = ROTOR_OK;
+        if (sq == ROTOR_OK && in.ops && h_n[k] > h_cap[k]) sq = ROTOR_ETRUNC;
+        if (out.status) out.status[q] = sq;
+        if (out.n_ops) out.n_ops[q] = (sq == ROTOR_OK || sq == ROTOR_ETRUNC) ? h_n[k] : -1;
+        out.costs[q] = sq == ROTOR_INFEASIBLE ? INFINITY : h_c[k];
+        if (sq != ROTOR_OK && sq != ROTOR_INFEASIBLE && sq != ROTOR_ETRUNC && !first_err) first_err = sq;
+        if (in.ops && h_n[k] > 0 && h_cap[k] > 0) {
+            const int64_t cnt = std::min(h_n[k], h_cap[k]);
+            CK(cudaMemcpyAsync(in.ops + in.ops_offsets[q], w + o_ops + h_off[k] * 8, cnt * 8, cudaMemcpyDeviceToHost,
+                               st));
+        }
+    }
+    CK(cudaStreamSynchronize(st));
+    if (first_err) return fail(first_err, "batched solve: a problem failed with status %d", first_err);
     return ROTOR_OK;
 }
 
@@ -343,8 +538,9 @@ int rotor_solve_ex(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int3
     const rotor_options o = opts_or_default(opt);
     Layout y = make_layout(L, slots, o);
     void *ws = d_workspace;
+    Lease lease;
     if (!ws) {
-        r = cached_workspace(y.total, &ws);
+        r = lease_workspace(0, y.total, lease, &ws);
         if (r) return r;
     } else if (workspace_bytes < y.total) {
         return fail(ROTOR_ENOMEM, "workspace too small: %llu < %zu", (unsigned long long)workspace_bytes, y.total);
@@ -371,6 +567,10 @@ int rotor_solve_ex(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int3
     CK(cudaMemcpyAsync((void *)dch.ob, chain->ob, n1 * 8, cudaMemcpyHostToDevice, st));
     r = enqueue_solve(dch, mem_limit, y, w, o, st, nullptr);
     if (r) return r;
+    if (lease.e) {
+        g_last.cache = lease.e;
+        g_last.cache_gen = lease.e->gen.load();
+    }
     struct {
         double cost;
         int64_t nops;
@@ -408,139 +608,74 @@ int rotor_solve(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int32_t
 }
 
 int rotor_solve_batch(const rotor_chain *chains, const int32_t *Ls, int32_t n_chains, const uint64_t *limits,
-                      int32_t n_limits, int32_t slots, const rotor_options *opt, void *stream, double *costs,
-                      rotor_op *ops, const int64_t *ops_offsets, const int64_t *ops_caps, int64_t *n_ops,
-                      int32_t *status) {
+                      int32_t n_limits, int32_t slots, const rotor_options *opt, const int32_t *devices,
+                      int32_t n_devices, void *stream, double *costs, rotor_op *ops, const int64_t *ops_offsets,
+                      const int64_t *ops_caps, int64_t *n_ops, int32_t *status) {
     if (!chains || !Ls || !limits || !costs || n_chains < 0 || n_limits < 0)
         return fail(ROTOR_EINPUT, "bad batch arguments");
     if (ops && (!ops_offsets || !ops_caps)) return fail(ROTOR_EINPUT, "ops requires ops_offsets and ops_caps");
     const int64_t P = (int64_t)n_chains * n_limits;
-    if (P == 0) return ROTOR_OK;
-    int L_max = 0;
     for (int i = 0; i < n_chains; i++) {
         int r = check_args(Ls[i], 1, slots);
         if (r) return r;
         r = check_host_chain(&chains[i], Ls[i]);
         if (r) return r;
-        L_max = std::max(L_max, (int)Ls[i]);
     }
     for (int64_t q = 0; q < P; q++)
         if (limits[q] == 0) return fail(ROTOR_EINPUT, "mem_limit must be > 0 (problem %lld)", (long long)q);
-    const rotor_options o = opts_or_default(opt);
-    cudaStream_t st = (cudaStream_t)stream;
-    int dev = 0, sms = 0;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-
-    // host staging: chains padded to a common stride, problem descriptors
-    const int64_t stride = L_max + 2;
-    std::vector<double> h_d(2 * n_chains * stride, 0.0);
-    std::vector<uint64_t> h_u(5 * n_chains * stride, 0);
-    for (int i = 0; i < n_chains; i++) {
-        const int n1 = Ls[i] + 1;
-        memcpy(&h_d[(0 * n_chains + i) * stride], chains[i].uf, n1 * 8);
-        memcpy(&h_d[(1 * n_chains + i) * stride], chains[i].ub, n1 * 8);
-        memcpy(&h_u[(0 * n_chains + i) * stride], chains[i].wx, n1 * 8);
-        memcpy(&h_u[(1 * n_chains + i) * stride], chains[i].wbx, n1 * 8);
-        memcpy(&h_u[(2 * n_chains + i) * stride], chains[i].wy, (n1 + 1) * 8);
-        memcpy(&h_u[(3 * n_chains + i) * stride], chains[i].of, n1 * 8);
-        memcpy(&h_u[(4 * n_chains + i) * stride], chains[i].ob, n1 * 8);
-    }
-    std::vector<int32_t> h_pc(P), h_L(Ls, Ls + n_chains);
-    std::vector<int64_t> h_off(P, 0), h_cap(P, 0);
-    int64_t total_ops = 0;
-    for (int64_t q = 0; q < P; q++) {
-        h_pc[q] = (int32_t)(q / n_limits);
-        if (ops) {
-            h_cap[q] = std::max<int64_t>(0, ops_caps[q]);
-            h_off[q] = total_ops;
-            total_ops += h_cap[q];
+    if (devices && n_devices < 1) return fail(ROTOR_EINPUT, "n_devices must be >= 1 with a device list");
+    // the workers: one per device-list entry (a device may be listed twice)
+    std::vector<int> workers;
+    int cur = 0;
+    CK(cudaGetDevice(&cur));
+    if (devices) {
+        int nvis = 0;
+        CK(cudaGetDeviceCount(&nvis));
+        for (int i = 0; i < n_devices; i++) {
+            if (devices[i] < 0 || devices[i] >= nvis) return fail(ROTOR_EINPUT, "bad device %d", devices[i]);
+            workers.push_back(devices[i]);
         }
+    } else if (n_devices < 0) {
+        int nvis = 0;
+        CK(cudaGetDeviceCount(&nvis));
+        for (int i = 0; i < nvis; i++) workers.push_back(i);
     }
-    // queue order: the longest chains first (cost ~ L^3 at a common S): the
-    // short tables fill the tail instead of a long one starting last
-    std::vector<int32_t> h_order(P);
-    for (int64_t q = 0; q < P; q++) h_order[q] = (int32_t)q;
-    std::stable_sort(h_order.begin(), h_order.end(),
-                     [&](int32_t x, int32_t y) { return Ls[h_pc[x]] > Ls[h_pc[y]]; });
-    // persistent k_batch CTAs (512 threads, 32 registers): four resident per SM,
-    // a full SM of threads (config 5: 1 per SM 86.4 ms, 2 59.0, 3 50.0 at 40
-    // registers / 47.5 at 32, 4 44.6; 256 threads x 6 62.6, x 7 60.6; 384 x 4
-    // 50.6; 128 x 12 91.2)
-    const int n_slots = (int)std::min<int64_t>(P, 4 * (int64_t)sms);
-    const size_t slot = rotor::batch_slot_bytes(L_max, slots);
-    // one device allocation (library cache): descriptors, outputs, ops, then the slot pool
-    size_t off = 0;
-    auto take = [&](size_t bytes) {
-        size_t r = off;
-        off += al(bytes);
-        return r;
-    };
-    const size_t o_d = take(h_d.size() * 8), o_u = take(h_u.size() * 8), o_pc = take(P * 4), o_L = take(n_chains * 4),
-                 o_lim = take(P * 8), o_off = take(P * 8), o_cap = take(P * 8), o_cost = take(P * 8),
-                 o_nops = take(P * 8), o_st = take(P * 4), o_ops = take((size_t)std::max<int64_t>(total_ops, 1) * 8),
-                 o_ctr = take(8), o_ord = take(P * 4), o_pool = take((size_t)n_slots * slot);
-    void *wsv = nullptr;
-    int r = cached_workspace(off, &wsv);
-    if (r) return r;
-    char *w = (char *)wsv;
-    CK(cudaMemcpyAsync(w + o_d, h_d.data(), h_d.size() * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(w + o_u, h_u.data(), h_u.size() * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(w + o_pc, h_pc.data(), P * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(w + o_L, h_L.data(), n_chains * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(w + o_lim, limits, P * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(w + o_off, h_off.data(), P * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(w + o_cap, h_cap.data(), P * 8, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(w + o_ord, h_order.data(), P * 4, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(w + o_ctr, 0, 8, st));
-    rotor::BatchArgs b{};
-    b.n_problems = (int)P;
-    b.S = slots;
-    b.restricted = o.restricted ? 1 : 0;
-    b.L_max = L_max;
-    b.prob_chain = (const int32_t *)(w + o_pc);
-    b.limits = (const uint64_t *)(w + o_lim);
-    b.chain_L = (const int32_t *)(w + o_L);
-    b.chain_stride = stride;
-    b.uf = (const double *)(w + o_d);
-    b.ub = (const double *)(w + o_d) + n_chains * stride;
-    b.wx = (const uint64_t *)(w + o_u);
-    b.wbx = (const uint64_t *)(w + o_u) + 1 * n_chains * stride;
-    b.wy = (const uint64_t *)(w + o_u) + 2 * n_chains * stride;
-    b.of = (const uint64_t *)(w + o_u) + 3 * n_chains * stride;
-    b.ob = (const uint64_t *)(w + o_u) + 4 * n_chains * stride;
-    b.pool = w + o_pool;
-    b.cost = (double *)(w + o_cost);
-    b.nops = (int64_t *)(w + o_nops);
-    b.status = (int32_t *)(w + o_st);
-    b.ops = ops ? (rotor_op *)(w + o_ops) : nullptr;
-    b.ops_off = (const int64_t *)(w + o_off);
-    b.ops_cap = (const int64_t *)(w + o_cap);
-    b.counter = (int *)(w + o_ctr);
-    b.order = (const int32_t *)(w + o_ord);
-    rotor::launch_batch(b, n_slots, st);
-    CK(cudaGetLastError());
-    std::vector<int64_t> h_n(P);
-    std::vector<int32_t> h_s(P);
-    CK(cudaMemcpyAsync(costs, w + o_cost, P * 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_n.data(), w + o_nops, P * 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_s.data(), w + o_st, P * 4, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    int first_err = ROTOR_OK;
-    for (int64_t q = 0; q < P; q++) {
-        int sq = h_s[q];
-        if (sq == ROTOR_OK && h_n[q] > h_cap[q] && ops) sq = ROTOR_ETRUNC;
-        if (status) status[q] = sq;
-        if (n_ops) n_ops[q] = (sq == ROTOR_OK || sq == ROTOR_ETRUNC) ? h_n[q] : -1;
-        if (sq == ROTOR_INFEASIBLE) costs[q] = INFINITY;
-        if (sq != ROTOR_OK && sq != ROTOR_INFEASIBLE && sq != ROTOR_ETRUNC && !first_err) first_err = sq;
-        if (ops && h_n[q] > 0 && h_cap[q] > 0) {
-            const int64_t cnt = std::min(h_n[q], h_cap[q]);
-            CK(cudaMemcpyAsync(ops + ops_offsets[q], w + o_ops + h_off[q] * 8, cnt * 8, cudaMemcpyDeviceToHost, st));
-        }
+    const BatchIn in{chains, Ls, n_chains, limits, n_limits, slots, opts_or_default(opt), ops, ops_offsets, ops_caps};
+    BatchOut out{costs, n_ops, status};
+    if (P == 0) return ROTOR_OK;
+    if (workers.empty()) {  // the current device, the caller's stream
+        std::vector<int64_t> idx(P);
+        std::iota(idx.begin(), idx.end(), 0);
+        return batch_on_device(in, idx, kBatchKind, (cudaStream_t)stream, out);
     }
-    CK(cudaStreamSynchronize(st));
-    if (first_err) return fail(first_err, "batched solve: a problem failed with status %d", first_err);
+    // LPT over the workers by nominal transitions; one host thread per worker,
+    // each with its own stream and (leased) workspace on its device
+    std::vector<double> wgt(P);
+    for (int64_t q = 0; q < P; q++) wgt[q] = rotor_transitions(Ls[q / n_limits], slots);
+    std::vector<int32_t> part(P);
+    rotor_partition_lpt(wgt.data(), (int32_t)P, (int32_t)workers.size(), part.data());
+    std::vector<std::vector<int64_t>> idx(workers.size());
+    for (int64_t q = 0; q < P; q++) idx[part[q]].push_back(q);
+    std::vector<int> rc(workers.size(), ROTOR_OK);
+    std::vector<std::string> msg(workers.size());
+    std::vector<std::thread> th;
+    for (size_t w = 0; w < workers.size(); w++) {
+        th.emplace_back([&, w]() {
+            if (idx[w].empty()) return;
+            cudaStream_t st = nullptr;
+            if (cudaSetDevice(workers[w]) != cudaSuccess ||
+                cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) {
+                rc[w] = fail(ROTOR_EDEVICE, "device %d: cannot create a stream", workers[w]);
+            } else {
+                rc[w] = batch_on_device(in, idx[w], kBatchKind + (int)w, st, out);
+                cudaStreamDestroy(st);
+            }
+            if (rc[w]) msg[w] = g_err;
+        });
+    }
+    for (auto &t : th) t.join();
+    for (size_t w = 0; w < workers.size(); w++)
+        if (rc[w]) return fail(rc[w], "device %d: %s", workers[w], msg[w].c_str());
     return ROTOR_OK;
 }
 
@@ -562,7 +697,7 @@ int rotor_partition_lpt(const double *weights, int32_t n_items, int32_t n_parts,
 }
 
 int rotor_export_tables(double *C_host, uint16_t *D_host, int64_t n_values) {
-    if (!g_last.valid) return fail(ROTOR_EINPUT, "no solve on this thread");
+    if (int r = check_last_alive()) return r;
     const Layout &y = g_last.y;
     const int64_t want = y.cells * (y.S + 1);
     if (n_values != want) return fail(ROTOR_EINPUT, "n_values %lld != %lld", (long long)n_values, (long long)want);
@@ -694,6 +829,8 @@ int rotor_sharded_finish(rotor_shard *h, void *stream, double *d_cost, rotor_op 
     g_last.device = h->device;
     g_last.stream = (cudaStream_t)stream;
     g_last.profiled = false;
+    g_last.counted = false;
+    g_last.cache = nullptr;  // the caller owns this workspace
     rotor::Problem p = h->p;
     // the precompute wrote its status into the workspace's result slot: carry it over
     CK(cudaMemcpyAsync(d_status, p.res_status, 4, cudaMemcpyDeviceToDevice, (cudaStream_t)stream));
@@ -708,8 +845,244 @@ int rotor_sharded_finish(rotor_shard *h, void *stream, double *d_cost, rotor_op 
     return ROTOR_OK;
 }
 
+// ---- one table sharded over a device list from one process (rotor_solve_sharded) ----
+namespace {
+// contiguous balanced ranges [lo, hi) of n items over k parts (the first n % k get one more)
+void tile_ranges(int n, int k, std::vector<int> &lo, std::vector<int> &hi) {
+    lo.resize(k);
+    hi.resize(k);
+    int a = 0;
+    for (int r = 0; r < k; r++) {
+        lo[r] = a;
+        a += n / k + (r < n % k ? 1 : 0);
+        hi[r] = a;
+    }
+}
+
+struct ShardRank {
+    int dev = 0;
+    Lease lease;
+    char *ws = nullptr;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_step = nullptr, ev_pack = nullptr, ev_copied = nullptr;
+    rotor::Problem p{};
+    rotor::TiledCtx ctx{};
+    double *send[2] = {nullptr, nullptr}, *recv = nullptr;
+};
+
+// host chain -> the staging area of a workspace (as rotor_solve_ex)
+int stage_chain(const rotor_chain *chain, int L, const Layout &y, char *w, cudaStream_t st, rotor_chain &dch) {
+    const size_t n1 = (size_t)L + 1;
+    const size_t seg = al(((size_t)y.n + 2) * 8);
+    char *stage = w + y.off_chain;
+    dch.uf = (const double *)(stage + 0 * seg);
+    dch.ub = (const double *)(stage + 1 * seg);
+    dch.wx = (const uint64_t *)(stage + 2 * seg);
+    dch.wbx = (const uint64_t *)(stage + 3 * seg);
+    dch.wy = (const uint64_t *)(stage + 4 * seg);
+    dch.of = (const uint64_t *)(stage + 5 * seg);
+    dch.ob = (const uint64_t *)(stage + 6 * seg);
+    CK(cudaMemcpyAsync((void *)dch.uf, chain->uf, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.ub, chain->ub, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.wx, chain->wx, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.wbx, chain->wbx, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.wy, chain->wy, (n1 + 1) * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.of, chain->of, n1 * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync((void *)dch.ob, chain->ob, n1 * 8, cudaMemcpyHostToDevice, st));
+    return ROTOR_OK;
+}
+
+int sharded_run(const rotor_chain *chain, int L, uint64_t M, int S, const rotor_options &o, std::vector<ShardRank> &rk,
+                int halo_mode, double *cost_out, rotor_op *ops, int64_t ops_cap, int64_t *n_ops_out) {
+    const int R = (int)rk.size();
+    const Layout y = make_layout(L, S, o);
+    const int nb = rotor::tiled_nb(y.n);
+    const int cap = (nb + R - 1) / R;  // most tiles one rank computes on one tile diagonal
+    const size_t tb = rotor::tiled_tile_bytes(S);
+    const size_t stage_bytes = halo_mode == 0 && R > 1 ? 3 * cap * tb : 0;
+    // per rank: device, leased workspace (+ the staging buffers of halo mode 0), stream, events, setup
+    for (int r = 0; r < R; r++) {
+        ShardRank &q = rk[r];
+        CK(cudaSetDevice(q.dev));
+        void *w = nullptr;
+        int e = lease_workspace(kShardKind + r, y.total + stage_bytes, q.lease, &w);
+        if (e) return e;
+        q.ws = (char *)w;
+        CK(cudaStreamCreateWithFlags(&q.st, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&q.ev_step, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&q.ev_pack, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&q.ev_copied, cudaEventDisableTiming));
+        if (stage_bytes) {
+            q.send[0] = (double *)(q.ws + y.total);
+            q.send[1] = (double *)(q.ws + y.total + cap * tb);
+            q.recv = (double *)(q.ws + y.total + 2 * cap * tb);
+        }
+        rotor_chain dch;
+        if ((e = stage_chain(chain, L, y, q.ws, q.st, dch))) return e;
+        q.p = make_problem(y, q.ws, o);
+        rotor::launch_precompute(dch, M, q.p, q.st);
+        rotor::launch_leaf(q.p, q.st);
+        CK(cudaGetLastError());
+        if (rotor::tiled_prepare(q.p, &q.ctx, q.st)) return fail(ROTOR_EDEVICE, "tiled setup failed on device %d", q.dev);
+        CK(cudaEventRecord(q.ev_copied, q.st));
+    }
+    std::vector<int> lo, hi;
+    for (int delta = 0; delta < nb; delta++) {
+        tile_ranges(nb - delta, R, lo, hi);
+        for (int r = 0; r < R; r++) {  // every rank: its share of the tiles of this diagonal
+            ShardRank &q = rk[r];
+            CK(cudaSetDevice(q.dev));
+            if (rotor::tiled_delta(q.p, &q.ctx, delta, lo[r], hi[r], q.st) < 0)
+                return fail(ROTOR_EDEVICE, "tiled step failed on device %d", q.dev);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(q.ev_step, q.st));
+        }
+        if (R == 1) continue;
+        if (halo_mode == 0) {  // pack -> peer copy -> unpack
+            const int b = delta & 1;
+            for (int r = 0; r < R; r++) {
+                ShardRank &q = rk[r];
+                if (hi[r] <= lo[r]) continue;
+                CK(cudaSetDevice(q.dev));
+                // send[b] was last read by the copies of delta - 2, which every
+                // receiver's stream ordered before its copies of delta - 1
+                for (int x = 0; x < R; x++)
+                    if (x != r) CK(cudaStreamWaitEvent(q.st, rk[x].ev_copied, 0));
+                rotor::tiled_pack(q.p, delta, lo[r], hi[r], q.send[b], 0, q.st);
+                CK(cudaGetLastError());
+                CK(cudaEventRecord(q.ev_pack, q.st));
+            }
+            for (int r = 0; r < R; r++) {
+                ShardRank &q = rk[r];
+                CK(cudaSetDevice(q.dev));
+                for (int x = 0; x < R; x++) {
+                    if (x == r || hi[x] <= lo[x]) continue;
+                    CK(cudaStreamWaitEvent(q.st, rk[x].ev_pack, 0));
+                    CK(cudaMemcpyPeerAsync(q.recv, q.dev, rk[x].send[b], rk[x].dev, (size_t)(hi[x] - lo[x]) * tb, q.st));
+                    rotor::tiled_pack(q.p, delta, lo[x], hi[x], q.recv, 1, q.st);
+                    CK(cudaGetLastError());
+                }
+                CK(cudaEventRecord(q.ev_copied, q.st));
+            }
+        } else {  // fused P2P halo: each rank pulls the owners' tiles through peer memory
+            for (int r = 0; r < R; r++) {
+                ShardRank &q = rk[r];
+                CK(cudaSetDevice(q.dev));
+                for (int x = 0; x < R; x++) {
+                    if (x == r || hi[x] <= lo[x]) continue;
+                    CK(cudaStreamWaitEvent(q.st, rk[x].ev_step, 0));
+                    rotor::tiled_pull(q.p, rk[x].p.C, delta, lo[x], hi[x], q.st);
+                    CK(cudaGetLastError());
+                }
+            }
+        }
+    }
+    // Algorithm 2 on the first rank's complete table
+    ShardRank &q0 = rk[0];
+    CK(cudaSetDevice(q0.dev));
+    rotor::launch_reconstruct(q0.p, q0.st);
+    CK(cudaGetLastError());
+    g_last.valid = true;
+    g_last.y = y;
+    g_last.p = q0.p;
+    g_last.device = q0.dev;
+    g_last.stream = q0.st;  // synchronised below; not used after the call
+    g_last.profiled = false;
+    g_last.counted = false;
+    g_last.cache = q0.lease.e;
+    g_last.cache_gen = q0.lease.e->gen.load();
+    struct {
+        double cost;
+        int64_t nops;
+        int32_t status;
+    } res;
+    CK(cudaMemcpyAsync(&res, q0.ws + y.off_res, 20, cudaMemcpyDeviceToHost, q0.st));
+    for (int r = 0; r < R; r++) {
+        CK(cudaSetDevice(rk[r].dev));
+        CK(cudaStreamSynchronize(rk[r].st));
+    }
+    CK(cudaSetDevice(q0.dev));
+    g_last.stream = nullptr;
+    if (cost_out) *cost_out = res.cost;
+    if (res.status == ROTOR_INFEASIBLE) {
+        if (n_ops_out) *n_ops_out = 0;
+        if (cost_out) *cost_out = INFINITY;
+        return fail(ROTOR_INFEASIBLE, "infeasible: no persistent schedule within the memory limit");
+    }
+    if (res.status != ROTOR_OK && res.status != ROTOR_ETRUNC)
+        return fail(res.status, "device phase failed with status %d", res.status);
+    if (n_ops_out) *n_ops_out = res.nops;
+    if (ops && ops_cap > 0 && res.nops > 0)
+        CK(cudaMemcpy(ops, q0.ws + y.off_ops, (size_t)std::min<int64_t>(res.nops, ops_cap) * sizeof(rotor_op),
+                      cudaMemcpyDeviceToHost));
+    if (ops && res.nops > ops_cap)
+        return fail(ROTOR_ETRUNC, "ops truncated: %lld > cap %lld", (long long)res.nops, (long long)ops_cap);
+    return ROTOR_OK;
+}
+}  // namespace
+
+int rotor_solve_sharded(const rotor_chain *chain, int32_t L, uint64_t mem_limit, int32_t slots,
+                        const rotor_options *opt, const int32_t *devices, int32_t n_devices, int32_t halo_mode,
+                        double *cost_out, rotor_op *ops, int64_t ops_cap, int64_t *n_ops_out) {
+    int r = check_args(L, mem_limit, slots);
+    if (r) return r;
+    if ((r = check_host_chain(chain, L))) return r;
+    if (halo_mode != 0 && halo_mode != 1) return fail(ROTOR_EINPUT, "halo_mode must be 0 or 1");
+    int nvis = 0, dev0 = 0;
+    CK(cudaGetDeviceCount(&nvis));
+    CK(cudaGetDevice(&dev0));
+    std::vector<int> devs;
+    if (devices) {
+        if (n_devices < 1) return fail(ROTOR_EINPUT, "n_devices must be >= 1 with a device list");
+        for (int i = 0; i < n_devices; i++) {
+            if (devices[i] < 0 || devices[i] >= nvis) return fail(ROTOR_EINPUT, "bad device %d", devices[i]);
+            devs.push_back(devices[i]);
+        }
+    } else {
+        const int k = n_devices < 0 ? nvis : n_devices;
+        if (k < 1 || k > nvis) return fail(ROTOR_EINPUT, "n_devices %d with %d visible devices", n_devices, nvis);
+        for (int i = 0; i < k; i++) devs.push_back(i);
+    }
+    // peer access between distinct devices (mode 1 needs it everywhere, else mode 0)
+    for (size_t i = 0; i < devs.size(); i++)
+        for (size_t j = 0; j < devs.size(); j++) {
+            if (devs[i] == devs[j]) continue;
+            int can = 0;
+            CK(cudaDeviceCanAccessPeer(&can, devs[i], devs[j]));
+            if (!can) {
+                halo_mode = 0;
+                continue;
+            }
+            CK(cudaSetDevice(devs[i]));
+            cudaError_t e = cudaDeviceEnablePeerAccess(devs[j], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else if (e != cudaSuccess) {
+                cudaSetDevice(dev0);
+                return fail(ROTOR_EDEVICE, "peer access %d -> %d: %s", devs[i], devs[j], cudaGetErrorString(e));
+            }
+        }
+    rotor_options o = opts_or_default(opt);
+    o.kernel = ROTOR_KERNEL_TILED;
+    o.keep_argmin = 0;
+    o.counters = 0;
+    o.profile = 0;
+    std::vector<ShardRank> rk(devs.size());
+    for (size_t i = 0; i < devs.size(); i++) rk[i].dev = devs[i];
+    r = sharded_run(chain, L, mem_limit, slots, o, rk, halo_mode, cost_out, ops, ops_cap, n_ops_out);
+    for (auto &q : rk) {  // on error too: wait for the work in flight, then free the streams / events
+        cudaSetDevice(q.dev);
+        if (q.st) cudaStreamSynchronize(q.st);
+        if (q.ev_step) cudaEventDestroy(q.ev_step);
+        if (q.ev_pack) cudaEventDestroy(q.ev_pack);
+        if (q.ev_copied) cudaEventDestroy(q.ev_copied);
+        if (q.st) cudaStreamDestroy(q.st);
+    }
+    cudaSetDevice(dev0);
+    return r;
+}
+
 int rotor_export_rows(const int32_t *s, const int32_t *t, int64_t n_rows, double *C_host) {
-    if (!g_last.valid) return fail(ROTOR_EINPUT, "no solve on this thread");
+    if (int r = check_last_alive()) return r;
     if (n_rows < 0 || (n_rows > 0 && (!s || !t || !C_host))) return fail(ROTOR_EINPUT, "bad export_rows arguments");
     const Layout &y = g_last.y;
     int dev = 0;
@@ -734,7 +1107,8 @@ int rotor_export_rows(const int32_t *s, const int32_t *t, int64_t n_rows, double
 
 int rotor_last_timings(rotor_timings *out) {
     if (!out) return fail(ROTOR_EINPUT, "out is NULL");
-    if (!g_last.valid || !g_last.profiled) return fail(ROTOR_EINPUT, "last solve was not profiled");
+    if (int r = check_last_alive()) return r;
+    if (!g_last.profiled) return fail(ROTOR_EINPUT, "last solve was not profiled");
     CK(cudaEventSynchronize(g_last.ev[3]));
     float a = 0, b = 0, c = 0;
     CK(cudaEventElapsedTime(&a, g_last.ev[0], g_last.ev[1]));
@@ -758,7 +1132,8 @@ int rotor_last_timings(rotor_timings *out) {
 
 int rotor_last_counters(rotor_counters *out) {
     if (!out) return fail(ROTOR_EINPUT, "out is NULL");
-    if (!g_last.valid || !g_last.counted) return fail(ROTOR_EINPUT, "last solve did not count (options.counters)");
+    if (int r = check_last_alive()) return r;
+    if (!g_last.counted) return fail(ROTOR_EINPUT, "last solve did not count (options.counters)");
     int dev = 0;
     CK(cudaGetDevice(&dev));
     if (dev != g_last.device) CK(cudaSetDevice(g_last.device));
@@ -789,17 +1164,21 @@ int rotor_last_counters(rotor_counters *out) {
 }
 
 int rotor_release(void) {
-    std::lock_guard<std::mutex> lk(g_cache_mu);
+    std::lock_guard<std::mutex> g(g_cache_mu);
     int dev0 = 0;
     cudaGetDevice(&dev0);
     for (auto &kv : g_cache) {
-        if (kv.second.first) {
-            cudaSetDevice(kv.first);
+        CacheEntry *e = kv.second.get();
+        std::lock_guard<std::mutex> lk(e->mu);  // waits for a call still using it
+        if (e->ptr) {
+            cudaSetDevice(kv.first.first);
             cudaDeviceSynchronize();
-            cudaFree(kv.second.first);
+            cudaFree(e->ptr);
+            e->ptr = nullptr;
+            e->bytes = 0;
         }
+        e->gen++;  // invalidates every last-solve record pointing at it
     }
-    g_cache.clear();
     cudaSetDevice(dev0);
     g_last.valid = false;
     return ROTOR_OK;

@@ -801,21 +801,27 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st, cudaEvent_t *mid_ev, in
 // and the exchange volume is half of sending both tables.
 size_t tiled_tile_bytes(int S) { return (size_t)tiled::TB * tiled::TB * (S + 1) * sizeof(double); }
 
-__global__ void k_tile_pack(Problem p, int delta, int tile_lo, double *buf, int unpack) {
+// mode 0: pack this table's tiles into buf; 1: unpack buf into this table;
+// 2: pull the tiles straight from another table of the same layout (`src`,
+// another device's C through peer memory: the fused P2P halo) into this one.
+__global__ void k_tile_pack(Problem p, int delta, int tile_lo, double *buf, const double *src, int mode) {
     using namespace tiled;
     const int n = p.n, W = p.S + 1;
     const int tile = blockIdx.z, a = blockIdx.y / TB, c = blockIdx.y % TB;
     const int I = tile_lo + tile, J = I + delta;
     const int s = I * TB + 1 + a, t = J * TB + 1 + c;
     if (s > n || t > n || s > t) return;
-    double *crow = p.C + cell_index(n, s, t) * p.pitch;
+    const int64_t row = cell_index(n, s, t);
+    double *crow = p.C + row * p.pitch;
+    const double *in = mode == 2 ? src + row * p.pitch : buf + (((int64_t)tile * TB + a) * TB + c) * W;
     double *packed = buf + (((int64_t)tile * TB + a) * TB + c) * W;
     const bool has_a = t < n;  // A(s, n) is never an operand
     const double u = has_a ? __dadd_rn(p.P[t], -p.P[s - 1]) : 0.0;
+    const int w = p.wx[s - 1];
     for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < W; m += gridDim.x * blockDim.x) {
-        if (unpack) {
-            const double v = packed[m];
-            store_final_c(p, cell_index(n, s, t), m, p.wx[s - 1], v);
+        if (mode) {
+            const double v = mode == 2 ? __ldcv(in + m) : in[m];  // .cv: the owner wrote it this diagonal
+            store_final_c(p, row, m, w, v);
             if (has_a) store_final_a(p, a_index(s, t), m, __dadd_rn(u, v));
         } else {
             packed[m] = crow[m];
@@ -826,7 +832,14 @@ __global__ void k_tile_pack(Problem p, int delta, int tile_lo, double *buf, int 
 int tiled_pack(const Problem &p, int delta, int tile_lo, int tile_hi, double *buf, int unpack, cudaStream_t st) {
     if (tile_hi <= tile_lo) return 0;
     dim3 grid(4, tiled::TB * tiled::TB, tile_hi - tile_lo);
-    k_tile_pack<<<grid, 256, 0, st>>>(p, delta, tile_lo, buf, unpack);
+    k_tile_pack<<<grid, 256, 0, st>>>(p, delta, tile_lo, buf, nullptr, unpack ? 1 : 0);
+    return 1;
+}
+
+int tiled_pull(const Problem &p, const double *src_C, int delta, int tile_lo, int tile_hi, cudaStream_t st) {
+    if (tile_hi <= tile_lo) return 0;
+    dim3 grid(4, tiled::TB * tiled::TB, tile_hi - tile_lo);
+    k_tile_pack<<<grid, 256, 0, st>>>(p, delta, tile_lo, nullptr, src_C, 2);
     return 1;
 }
 

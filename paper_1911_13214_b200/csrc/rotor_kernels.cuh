@@ -53,5 +53,8 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st);
 int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int tile_hi, cudaStream_t st);
 size_t tiled_tile_bytes(int S);
 int tiled_pack(const Problem &p, int delta, int tile_lo, int tile_hi, double *buf, int unpack, cudaStream_t st);
+// copy the tiles' C rows from another table of the same layout (e.g. a peer
+// device's, through peer memory) and rebuild A and the shadows (the P2P halo)
+int tiled_pull(const Problem &p, const double *src_C, int delta, int tile_lo, int tile_hi, cudaStream_t st);
 
 }  // namespace rotor

@@ -155,13 +155,26 @@ def shard(weights, world: int):
 
 
 def _default_solver(chains, limits, slots, pairs, **opts):
-    """Solve the listed (chain index, limit index) pairs on this rank's GPU."""
-    from . import solve
+    """Solve the listed (chain index, limit index) pairs on this rank's GPU with the
+    fused batched kernel (rotor_solve_batch): the pairs are grouped per chain into
+    one chains x limits grid, ragged rows padded by repeating their last limit
+    (the padding's results are dropped)."""
+    from . import solve_batch
 
+    if not pairs:
+        return []
+    rows = {}
+    for i, j in pairs:
+        rows.setdefault(i, []).append(j)
+    order = sorted(rows)
+    width = max(len(v) for v in rows.values())
+    grid = [[limits[i][j] for j in rows[i]] + [limits[i][rows[i][-1]]] * (width - len(rows[i])) for i in order]
+    costs, status, n_ops, ops = solve_batch([chains[i] for i in order], grid, slots, with_ops=True, **opts)
+    where = {(i, j): (a, b) for a, i in enumerate(order) for b, j in enumerate(rows[i])}
     out = []
     for i, j in pairs:
-        r = solve(chains[i], limits[i][j], slots, **opts)
-        out.append((r.status, r.cost, r.n_ops, r.ops))
+        a, b = where[(i, j)]
+        out.append((int(status[a, b]), float(costs[a, b]), int(n_ops[a, b]), ops[a * width + b]))
     return out
 
 

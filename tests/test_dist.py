@@ -93,3 +93,34 @@ def test_lpt_shards_balanced():
         part = shard(w, world)
         loads = np.bincount(part, weights=w, minlength=world)
         assert loads.max() / loads.mean() < 1.01
+
+
+def test_default_solver_grouping(monkeypatch):
+    """dist's default per-rank solver packs a rank's (chain, limit) pairs into one
+    padded chains x limits grid for the fused rotor_solve_batch, and maps every
+    result back to its pair (a fake batch returns the limit as the cost)."""
+    import __graft_entry__ as ge
+
+    ge.build_library()
+    import numpy as np
+
+    import paper_1911_13214_b200 as R
+    from paper_1911_13214_b200 import dist as D
+
+    calls = []
+
+    def fake(chains, grid, slots, with_ops=False, **opts):
+        calls.append(len(chains))
+        g = np.array(grid, dtype=np.float64)
+        st = np.zeros(g.shape, dtype=np.int32)
+        nops = np.arange(g.size, dtype=np.int64).reshape(g.shape)
+        return g, st, nops, [np.full((1, 2), k, dtype=np.int32) for k in range(g.size)]
+
+    monkeypatch.setattr(R, "solve_batch", fake)
+    chains = ["c0", "c1", "c2"]
+    limits = [[10, 11, 12, 13], [20, 21, 22, 23], [30, 31, 32, 33]]
+    pairs = [(2, 1), (0, 3), (2, 0), (0, 0), (2, 3), (1, 2)]
+    out = D._default_solver(chains, limits, 100, pairs)
+    assert calls == [3]
+    assert [c for _, c, _, _ in out] == [limits[i][j] for i, j in pairs]
+    assert D._default_solver(chains, limits, 100, []) == []

@@ -409,3 +409,97 @@ def test_counters(R, oracle_mod):
     assert 0 < c["middle_nominal"] < c["nominal"]
     assert c["evaluated"] == 512.0 * c["quadrant_compares"] + 2048.0 * c["exact_splits"] + c["dependent_nominal"]
     assert c["evaluated"] < c["nominal"]
+
+
+@pytest.mark.parametrize("halo_mode", [0, 1])
+@pytest.mark.parametrize("ranks", [2, 3])
+def test_solve_sharded_device_list(R, oracle_mod, halo_mode, ranks):
+    """rotor_solve_sharded (one process, a device list; §8(b)/(e) 2): config 2 and
+    config 3 with the table sharded over `ranks` entries of device 0 (each entry
+    its own workspace and stream; tiles exchanged by pack + peer copy or by the
+    fused peer pull) — full table, cost and schedule bit-identical to the oracle."""
+    O = oracle_mod
+    for p in (G.config2(), G.config3()):
+        ch = p.chain
+        o = O.OracleSolve(ch, p.mem_limit, p.slots, threads=O.max_threads(), keep_d=False)
+        res = R.solve_sharded(ch, p.mem_limit, p.slots, [0] * ranks, halo_mode=halo_mode)
+        assert res.status == R.OK and res.cost == o.cost
+        assert res.op_list() == o.reconstruct()
+        C, _ = R.export_tables(ch.L + 1, p.slots, D=False)
+        assert_tables_equal(C, o.table_view(), f"sharded x{ranks} halo {halo_mode} {ch.name}")
+    R.release()
+
+
+def test_solve_sharded_config4_golden(R):
+    """Config 4 sharded over two entries of device 0 (2 x 48.5 GB workspaces),
+    fused peer pull: cost bits, schedule and top row equal the oracle golden."""
+    import os
+
+    import table_hash as TH
+
+    g = TH.read_golden(os.path.join(os.path.dirname(__file__), "golden", "cfg4_L1000_S4000.txt"))
+    p = G.config4()
+    n = p.chain.L + 1
+    res = R.solve_sharded(p.chain, p.mem_limit, p.slots, [0, 0], halo_mode=1)
+    assert res.status == R.OK
+    assert int(bits(np.array([res.cost]))[0]) == int(g["cost"], 16)
+    assert res.op_list() == [(x >> 32, x & 0xFFFFFFFF) for x in g["ops"]]
+    top = R.export_rows([(1, n)], p.slots)[0]
+    assert [int(x) for x in bits(top)] == g["top"]
+    R.release()
+
+
+def test_batch_device_list(R, oracle_mod):
+    """rotor_solve_batch over a device list (§8(b)/(e) 1: LPT-split problems, one
+    worker thread per entry; here three entries of device 0) equals the
+    single-device batch bit for bit, and the oracle on a sample; costs-only mode
+    reports OK (not ETRUNC) for feasible problems."""
+    O = oracle_mod
+    chains, limits, S = G.config5(n_limits=16)
+    c1, s1, n1, o1 = R.solve_batch(chains, limits, S, with_ops=True)
+    c3, s3, n3, o3 = R.solve_batch(chains, limits, S, with_ops=True, devices=[0, 0, 0])
+    assert np.array_equal(bits(c1), bits(c3)) and np.array_equal(s1, s3) and np.array_equal(n1, n3)
+    assert all(np.array_equal(a, b) for a, b in zip(o1, o3))
+    c0, s0, _, _ = R.solve_batch(chains, limits, S, with_ops=False, devices=[0, 0])
+    assert np.array_equal(bits(c0), bits(c1))
+    assert set(np.unique(s0)) <= {R.OK, R.INFEASIBLE} and np.array_equal(s0 == R.OK, s1 == R.OK)
+    for i in range(0, len(chains), 3):
+        for j in (0, 7, 15):
+            o = O.OracleSolve(chains[i], limits[i][j], S)
+            assert (math.isinf(o.cost) and math.isinf(c3[i, j])) or c3[i, j] == o.cost
+
+
+def test_cached_workspace_threads(R, oracle_mod):
+    """Library workspaces are leased per call: two threads solving concurrently on
+    one device with the default (cached) workspace both get the oracle's result,
+    and exporting tables that a later call reused is refused, not misread."""
+    import threading
+
+    O = oracle_mod
+    p = G.config2()
+    ch = p.chain
+    limits = [p.mem_limit, p.mem_limit // 2]
+    want = [O.OracleSolve(ch, M, p.slots).cost for M in limits]
+    got = [None, None]
+    errs = []
+
+    def run(k):
+        try:
+            for _ in range(6):
+                got[k] = R.solve(ch, limits[k], p.slots).cost
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(k,)) for k in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs and got == want and want[0] != want[1]
+    R.solve(ch, p.mem_limit, p.slots)
+    R.export_rows([(1, 2)], p.slots)  # still this thread's tables
+    other = threading.Thread(target=lambda: R.solve(ch, limits[1], p.slots))
+    other.start()
+    other.join()
+    with pytest.raises(R.RotorError):
+        R.export_rows([(1, 2)], p.slots)
