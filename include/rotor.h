@@ -82,7 +82,9 @@ typedef struct {
     int32_t keep_argmin; /* 1: record D (uint16 argmin) during the fill (wavefront kernel only) */
     int32_t profile;     /* 1: time the phases with CUDA events (see rotor_last_timings) */
     int32_t counters;    /* 1: count the pruned middle kernel's work (see rotor_last_counters) */
-    int32_t reserved[3];
+    int32_t schedule;    /* tiled fill: 0 = tile DAG over several streams (default),
+                            1 = diagonal by diagonal on the caller's stream (middle launches timed) */
+    int32_t reserved[2];
 } rotor_options;
 
 /* Default options: all zero (unrestricted, auto kernel, no D, no profiling). */

@@ -47,7 +47,8 @@ class rotor_op(ctypes.Structure):
 class rotor_options(ctypes.Structure):
     _fields_ = [
         ("restricted", ctypes.c_int32), ("kernel", ctypes.c_int32), ("keep_argmin", ctypes.c_int32),
-        ("profile", ctypes.c_int32), ("counters", ctypes.c_int32), ("reserved", ctypes.c_int32 * 3),
+        ("profile", ctypes.c_int32), ("counters", ctypes.c_int32), ("schedule", ctypes.c_int32),
+        ("reserved", ctypes.c_int32 * 2),
     ]
 
 
@@ -134,8 +135,13 @@ def _check(r: int, allow=(OK,)):
     return r
 
 
-def _options(restricted=False, kernel="auto", keep_argmin=False, profile=False, counters=False) -> rotor_options:
+SCHEDULES = {"dag": 0, "diagonal": 1}
+
+
+def _options(restricted=False, kernel="auto", keep_argmin=False, profile=False, counters=False,
+             schedule="dag") -> rotor_options:
     o = rotor_options()
+    o.schedule = SCHEDULES[schedule] if isinstance(schedule, str) else int(schedule)
     o.counters = 1 if counters else 0
     o.restricted = 1 if restricted else 0
     o.kernel = KERNELS[kernel] if isinstance(kernel, str) else int(kernel)

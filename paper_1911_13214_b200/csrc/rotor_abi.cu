@@ -304,14 +304,15 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
         g_last.mid_n = 0;
         int cap = 0;
         if (o.profile) {
-            cap = rotor::tiled_nb(y.n);
+            const int nb = rotor::tiled_nb(y.n);
+            cap = nb * (nb - 1) / 2;  // middle launches: one per diagonal, or one per tile (DAG schedule)
             while ((int)g_last.mid_ev.size() < 2 * cap) {
                 cudaEvent_t e;
                 CK(cudaEventCreate(&e));
                 g_last.mid_ev.push_back(e);
             }
         }
-        fill = rotor::launch_fill_tiled(p, st, cap ? g_last.mid_ev.data() : nullptr, cap, &g_last.mid_n);
+        fill = rotor::launch_fill_tiled(p, st, o.schedule, cap ? g_last.mid_ev.data() : nullptr, cap, &g_last.mid_n);
         if (fill < 0) {
             cudaError_t e = cudaGetLastError();
             return fail(ROTOR_EDEVICE, "tiled fill launch failed: %s", cudaGetErrorString(e));

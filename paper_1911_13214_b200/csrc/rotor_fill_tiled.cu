@@ -26,6 +26,9 @@
 #include <string.h>
 #include <limits.h>
 
+#include <map>
+#include <vector>
+
 #include "rotor_common.cuh"
 #include "rotor_kernels.cuh"
 
@@ -722,8 +725,9 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
 }
 
 // Middle + dependent phase of the tiles I in [tile_lo, tile_hi) of tile
-// diagonal delta.  Returns the number of kernels launched.
-int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int tile_hi, cudaStream_t st) {
+// diagonal delta; `phase` counts the leaf launches that used the flags of
+// these tile rows (the look-back epochs).  Returns the number of kernels launched.
+int tiled_delta_ep(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int tile_hi, cudaStream_t st, int &phase) {
     using namespace tiled;
     if (tile_hi <= tile_lo) return 0;
     int launches = 0;
@@ -774,18 +778,71 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
         if (timed) cudaEventRecord(ctx->mid_ev[2 * ctx->mid_n++ + 1], st);
         launches++;
     }
-    return launches + launch_dependent(p, delta, tile_lo, tile_hi, st, p.flags, ctx->phase_id);
+    return launches + launch_dependent(p, delta, tile_lo, tile_hi, st, p.flags, phase);
 }
 
+int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int tile_hi, cudaStream_t st) {
+    return tiled_delta_ep(p, ctx, delta, tile_lo, tile_hi, st, ctx->phase_id);
+}
+
+namespace {
+// Per-thread, per-device streams and events of the tile-DAG schedule.
+struct DagRes {
+    std::vector<cudaStream_t> st;
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t start = nullptr;
+};
+DagRes *dag_res(int nb) {
+    static thread_local std::map<int, DagRes> res;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    DagRes &r = res[dev];
+    if (!r.start && cudaEventCreateWithFlags(&r.start, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    while ((int)r.st.size() < nb) {
+        cudaStream_t s;
+        cudaEvent_t e;
+        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        r.st.push_back(s);
+        r.ev.push_back(e);
+    }
+    return &r;
+}
+}  // namespace
+
+// The whole fill.  schedule 1: diagonal by diagonal on `st` (every launch
+// covers all tiles of a tile diagonal; the middle launches can be timed).
+// schedule 0 (default): the tile DAG.  Tile (I, J) depends only on tiles of
+// its row I and column J with smaller J - I (Theorem 1 reads strictly shorter
+// intervals); its row's tiles run in order on stream I, and its
+// column's through tile (I+1, J), whose own dependencies cover the rest, so
+// each tile task waits on ONE event: (I+1, J) done.  Tiles of different rows
+// then overlap — a tile's latency-bound dependent phase with other tiles'
+// middles — instead of every diagonal ending in a device-wide barrier.
 // Returns the number of kernels launched, or -1 on a launch/setup error.
-int launch_fill_tiled(const Problem &p, cudaStream_t st, cudaEvent_t *mid_ev, int mid_cap, int *mid_n) {
+int launch_fill_tiled(const Problem &p, cudaStream_t st, int schedule, cudaEvent_t *mid_ev, int mid_cap, int *mid_n) {
     TiledCtx ctx;
     if (tiled_prepare(p, &ctx, st)) return -1;
     ctx.mid_ev = mid_ev;
     ctx.mid_cap = mid_cap;
     const int nb = tiled_nb(p.n);
     int launches = 0;
-    for (int delta = 0; delta < nb; delta++) launches += tiled_delta(p, &ctx, delta, 0, nb - delta, st);
+    DagRes *r = schedule == 0 ? dag_res(nb) : nullptr;
+    if (!r) {
+        for (int delta = 0; delta < nb; delta++) launches += tiled_delta(p, &ctx, delta, 0, nb - delta, st);
+    } else {
+        std::vector<int> phase(nb, 0);  // (middle launches are timed on their own streams; they overlap)
+        cudaEventRecord(r->start, st);
+        for (int I = 0; I < nb; I++) cudaStreamWaitEvent(r->st[I], r->start, 0);
+        for (int delta = 0; delta < nb; delta++)
+            for (int I = 0; I + delta < nb; I++) {
+                // (I+1, I+delta) is the latest record of ev[I+1]: row I+1 is enqueued after row I
+                if (delta >= 1) cudaStreamWaitEvent(r->st[I], r->ev[I + 1], 0);
+                launches += tiled_delta_ep(p, &ctx, delta, I, I + 1, r->st[I], phase[I]);
+                cudaEventRecord(r->ev[I], r->st[I]);
+            }
+        for (int I = 0; I < nb; I++) cudaStreamWaitEvent(st, r->ev[I], 0);
+    }
     if (mid_n) *mid_n = ctx.mid_n;
     return launches;
 }

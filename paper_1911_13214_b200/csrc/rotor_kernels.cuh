@@ -32,7 +32,8 @@ void launch_batch(const BatchArgs &b, int n_slots, cudaStream_t st);
 
 // Tiled fill (rotor_fill_tiled.cu). Returns the number of kernels launched (-1: setup error).
 // mid_ev (optional, 2 * mid_cap events): recorded around each middle-kernel launch
-int launch_fill_tiled(const Problem &p, cudaStream_t st, cudaEvent_t *mid_ev = nullptr, int mid_cap = 0,
+// schedule: 0 = the tile DAG over several streams (default), 1 = diagonal by diagonal on st
+int launch_fill_tiled(const Problem &p, cudaStream_t st, int schedule, cudaEvent_t *mid_ev = nullptr, int mid_cap = 0,
                       int *mid_n = nullptr);
 size_t tiled_extra_bytes(int L, int S);
 

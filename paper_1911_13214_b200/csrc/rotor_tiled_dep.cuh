@@ -437,7 +437,9 @@ __global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf(Problem p,
     sub_at(delta, e, sub % cnt, alpha, gamma);
     const int I = tile_lo + sub / cnt;
     const int m = q * LEAF_M + threadIdx.x;
-    int *my_flags = flags + (int64_t)sub * n_chunks;
+    // flags of this sub-tile: indexed by the ABSOLUTE tile row I (tiles of
+    // different launches may be in flight at once, each with its own epochs)
+    int *my_flags = flags + ((int64_t)I * NSB + sub % cnt) * n_chunks;
     (void)n;
     for (int r = SB - 1; r >= 0; r--) {
         if (r < SB - 1) {
@@ -612,7 +614,7 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
     const int m = q * LEAF_M + threadIdx.x;
     const bool fresh = (delta == 0);
     const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
-    int *my_flags = flags + (int64_t)sub * n_chunks;
+    int *my_flags = flags + ((int64_t)I * NSB + sub % cnt) * n_chunks;  // by absolute tile row (see k_sub_leaf)
     leaf_tab_fill(p, s0, t0, q * LEAF_M, LEAF_M, T);
     const int q_lo = T.q_lo;
     if (RS) {
@@ -669,7 +671,7 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
 // both the right-range operands and its own results in shared memory, 147 vs
 // 119 ms at the time; profiles/r01_tiled_v4.md, r01_tiled_v5.md.)
 
-// Flags of the leaf look-back: one int per (sub-tile of a phase, m-chunk).
+// Flags of the leaf look-back: one int per (tile row I, sub-tile of a phase, m-chunk).
 inline size_t leaf_flag_bytes(int L, int S) {
     const int nb = (L + 1 + TB - 1) / TB;
     const int chunks = (S + 1 + LEAF_M - 1) / LEAF_M;

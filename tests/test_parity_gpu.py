@@ -503,3 +503,23 @@ def test_cached_workspace_threads(R, oracle_mod):
     other.join()
     with pytest.raises(R.RotorError):
         R.export_rows([(1, 2)], p.slots)
+
+
+@pytest.mark.parametrize("schedule", ["diagonal", "dag"])
+def test_tiled_schedules(R, oracle_mod, schedule):
+    """Both schedules of the tiled fill (the tile DAG over several streams, the
+    default; diagonal by diagonal on one stream) give the oracle's full table,
+    cost and schedule — config 3 and chains whose lengths end mid-tile."""
+    O = oracle_mod
+    cases = [G.config3()]
+    rng = G.SplitMix64(911)
+    for L in (33, 95, 160):
+        ch = G.random_chain(rng, L, real_times=True, big=True)
+        cases.append(G.Problem(ch, mem_limit=max(1, int(sum(int(x) for x in ch.wbx) * 0.2)), slots=97, name=f"r{L}"))
+    for p in cases:
+        ch = p.chain
+        o = O.OracleSolve(ch, p.mem_limit, p.slots, threads=O.max_threads(), keep_d=False)
+        res = R.solve(ch, p.mem_limit, p.slots, kernel="tiled", schedule=schedule)
+        C, _ = R.export_tables(ch.L + 1, p.slots, D=False)
+        assert_tables_equal(C, o.table_view(), f"{schedule} {p.name}")
+        assert res.cost == o.cost and res.op_list() == (o.reconstruct() or [])
