@@ -134,6 +134,7 @@ rotor::Problem make_problem(const Layout &y, char *ws, const rotor_options &o) {
     p.srows = y.cells + rotor::kPadRows;
     p.counters = (y.has_A && o.counters) ? (unsigned long long *)(ws + y.off_ctr) : nullptr;
     p.flags = y.has_A ? (int *)(ws + y.off_tiled) : nullptr;
+    p.mlist = y.has_A ? (uint16_t *)(ws + y.off_tiled + rotor::tiled_list_offset(y.L, y.S)) : nullptr;
     p.res_cost = (double *)(ws + y.off_res);
     p.res_nops = (int64_t *)(ws + y.off_res + 8);
     p.res_status = (int32_t *)(ws + y.off_res + 16);

@@ -37,6 +37,7 @@ struct Problem {
     uint16_t *D;  // nullable
     double *A;    // nullable: A(s,c,m) = fl(fl(P[c]-P[s-1]) + C(s,c,m)), row a_index(s,c) (tiled fill)
     int *flags;   // nullable: tiled fill's leaf look-back flags (tiled_extra_bytes)
+    uint16_t *mlist;  // nullable: the pruned middle's fired-split lists (tiled_extra_bytes)
     // nullable (tiled fill): fp32 round-down shadows of C and A in the m-chunked
     // layout of shadow_index() over srows rows, read by the pruned middle
     // kernel's lower-bound filter.  C32 is stored PRE-SHIFTED by the shift of

@@ -147,6 +147,22 @@ constexpr int INT_MIN_COLS = 0;  // register-tile columns j >= RT - INT_MIN_COLS
 // 16 warps (thread = one m, a 4x8 (s,t) register tile); thread 0 also issues
 // the 2*KC TMA boxes of each stage (full/empty mbarrier ring).
 // ---------------------------------------------------------------------------
+// The middle's per-(tile row I, 32-m chunk, warp) fired-split lists, read by
+// the sub-product of the dependent phase (the warp's 8 x 8 cells are exactly
+// one dependent-phase sub-tile): [0] = count, or MLIST_OVERFLOW when the
+// middle evaluated its splits itself and wrote the exact partial; [1..count] =
+// split index f (s' = i0 + TB + f).  Per tile ROW: the tiles of one row run
+// in order (DAG: one stream per row; diagonal schedule: diagonal by diagonal).
+constexpr int MLIST_STRIDE = 32, MLIST_CAP = MLIST_STRIDE - 1;
+constexpr uint16_t MLIST_OVERFLOW = 0xFFFF;
+__host__ __device__ inline int n_mc32(int S) { return (S + 1 + kSW - 1) / kSW; }
+__host__ __device__ inline int64_t mlist_index(int n_mc, int I, int q, int w) {
+    return (((int64_t)I * n_mc + q) * (CONSUMERS / 32) + w) * MLIST_STRIDE;
+}
+inline size_t mlist_bytes(int L, int S) {
+    return (size_t)((L + 1 + TB - 1) / TB) * n_mc32(S) * (CONSUMERS / 32) * MLIST_STRIDE * sizeof(uint16_t);
+}
+
 template <int KC_, int STAGES_>
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmC, Problem p,
@@ -274,6 +290,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int I = tile_lo + item / n_mc, J = I + delta;
     const int i0 = I * TB + 1, j0 = J * TB + 1;
     const int m = (item % n_mc) * TM + mi;
+    // the partials below are final for the middle range: tell the sub-product
+    // (fired-split lists of the pruned kernel) to read them
+    if (tid < CONSUMERS / 32) p.mlist[mlist_index(n_mc32(p.S), I, (item % n_mc) * TM / kSW, tid)] = MLIST_OVERFLOW;
     if (m <= p.S) {
 #pragma unroll
         for (int i = 0; i < RS; i++) {
@@ -308,6 +327,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 constexpr int TMW = kSW, RW = 8;
 constexpr int BOX = TB * TMW;                    // floats per operand box (4 KB)
 constexpr int FMAX_CAP = 2048;                   // fired splits a warp can record per item (see fmax)
+
 
 // Exact pass of a warp over the splits it recorded for one item: s' = sp_lo +
 // flist[f], f < nf — or, if the list overflowed (nf > fmax), every split
@@ -598,7 +618,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         __syncwarp();
         lap(c_loop);
-        exact_flush(p, flist, nf, fmax, I * TB + 1 + TB, iters * KC, s_0, t_0, SS, m, mc, wxp);  // the item's exact pass
+        // the item's fired splits go to the dependent phase's sub-product, which
+        // evaluates them exactly with its own splits; only an overflowing list
+        // is evaluated here (and its exact partial written)
+        uint16_t *gl = p.mlist + mlist_index(n_mc, I, item % n_mc, warp);
+        if (SS == 1 && nf <= MLIST_CAP) {
+            if (lane < nf) gl[1 + lane] = flist[lane];
+            if (lane == 0) gl[0] = (uint16_t)nf;
+        } else {
+            exact_flush(p, flist, nf, fmax, I * TB + 1 + TB, iters * KC, s_0, t_0, SS, m, mc, wxp);
+            if (lane == 0) gl[0] = MLIST_OVERFLOW;
+        }
         __syncwarp();
         lap(c_flush);
     }
@@ -679,8 +709,10 @@ void launch_wide(const Problem &p, int delta, int tile_lo, int nt, int coarse, i
 
 }  // namespace tiled
 
-// Scratch of the tiled fill beyond the A table (which is part of the Layout): the leaf flags.
-size_t tiled_extra_bytes(int L, int S) { return tiled::leaf_flag_bytes(L, S); }
+// Scratch of the tiled fill beyond the A table (which is part of the Layout):
+// the leaf flags, then (256-byte aligned) the middle's fired-split lists.
+size_t tiled_list_offset(int L, int S) { return (tiled::leaf_flag_bytes(L, S) + 255) & ~(size_t)255; }
+size_t tiled_extra_bytes(int L, int S) { return tiled_list_offset(L, S) + tiled::mlist_bytes(L, S); }
 
 int tiled_nb(int n) { return (n + tiled::TB - 1) / tiled::TB; }
 
@@ -785,6 +817,11 @@ int tiled_delta(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int til
     return tiled_delta_ep(p, ctx, delta, tile_lo, tile_hi, st, ctx->phase_id);
 }
 
+inline int env_int(const char *name, int dflt) {
+    const char *e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 namespace {
 // Per-thread, per-device streams and events of the tile-DAG schedule.
 struct DagRes {
@@ -798,10 +835,16 @@ DagRes *dag_res(int nb) {
     if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
     DagRes &r = res[dev];
     if (!r.start && cudaEventCreateWithFlags(&r.start, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    static const int prio = env_int("ROTOR_DAG_PRIO", 1);  // rows with lower I first (127.4 vs 129.1 ms per solve; 0: all equal)
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
     while ((int)r.st.size() < nb) {
         cudaStream_t s;
         cudaEvent_t e;
-        if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        const int i = (int)r.st.size();
+        // priority levels spread over the rows: row 0 the highest
+        const int pr = prio ? greatest + (least - greatest) * i / max(1, nb - 1) : least;
+        if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, pr) != cudaSuccess) return nullptr;
         if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
         r.st.push_back(s);
         r.ev.push_back(e);

@@ -36,6 +36,7 @@ void launch_batch(const BatchArgs &b, int n_slots, cudaStream_t st);
 int launch_fill_tiled(const Problem &p, cudaStream_t st, int schedule, cudaEvent_t *mid_ev = nullptr, int mid_cap = 0,
                       int *mid_n = nullptr);
 size_t tiled_extra_bytes(int L, int S);
+size_t tiled_list_offset(int L, int S);  // of the middle's fired-split lists within the extra bytes
 
 // Pieces of the tiled fill for a sharded (multi-rank) solve.
 struct TiledCtx {

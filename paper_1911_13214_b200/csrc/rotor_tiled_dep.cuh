@@ -45,105 +45,7 @@ __host__ __device__ inline void sub_at(int delta, int e, int q, int &alpha, int 
 // otherwise written by an earlier tile diagonal -> plain (L1-cacheable).
 __device__ __forceinline__ double ld(const double *p, bool fresh) { return fresh ? __ldcg(p) : *p; }
 
-// Product for one sub-tile: a warp covers 16 consecutive m; lane = (m, half),
-// each lane an SB x (SB/2) register tile (columns half*4 .. half*4+3), so the
-// kernel fits ~100 registers (occupancy for the load latency); the operand
-// loads of split k+1 are issued before the arithmetic of split k.
-constexpr int PH = SB / 2;  // columns per lane
-
-template <int MINB>
-__global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product(Problem p, int delta, int e, int tile_lo,
-                                                                int ntiles) {
-    const int n = p.n, S = p.S;
-    const int cnt = sub_count(delta, e);
-    const int n_mg = (S + 1 + 15) / 16;
-    const int item = (blockIdx.x * DEP_THREADS + threadIdx.x) >> 5;
-    if (item >= ntiles * cnt * n_mg) return;
-    const int lane = threadIdx.x & 31;
-    const int m = (item % n_mg) * 16 + (lane & 15);
-    const int jh = (lane >> 4) * PH;  // first column of this lane
-    const int rest = item / n_mg;
-    int alpha, gamma;
-    sub_at(delta, e, rest % cnt, alpha, gamma);
-    const int I = tile_lo + rest / cnt, J = I + delta;
-    const int i0 = I * TB + 1, j0 = J * TB + 1;
-    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
-    // split ranges and the freshness of their operands
-    int lo1, hi1, lo2 = 1, hi2 = 0;
-    bool fA1, fC1, fA2 = true, fC2 = true, partial;
-    if (delta == 0) {  // sub-blocks alpha+1 .. gamma-1, all inside this tile
-        lo1 = i0 + SB * (alpha + 1);
-        hi1 = t0 - 1;
-        fA1 = fC1 = true;
-        partial = false;
-    } else {
-        lo1 = s0 + SB;  // sub-blocks alpha+1 .. NSB-1 of I
-        hi1 = i0 + TB - 1;
-        fA1 = false;  // A(s, s'-1) in tile (I,I)
-        fC1 = true;   // C(s', t) in this tile
-        lo2 = j0;     // sub-blocks 0 .. gamma-1 of J
-        hi2 = t0 - 1;
-        fA2 = true;   // A(s, s'-1) in this tile (or (I,J-1) for s' = j0: earlier, .cg is still correct)
-        fC2 = false;  // C(s', t) in tile (J,J)
-        partial = delta >= 2;
-    }
-    if (hi1 < lo1 && hi2 < lo2) return;     // uniform over the warp
-    if (s0 > n || t0 > n) return;           // sub-tiles past the last stage have no cells (uniform)
-    // the shifts of both split ranges, staged per warp (no global load on the split loop's critical path)
-    __shared__ int wxs[DEP_THREADS / 32][2 * TB];
-    int *ws = wxs[threadIdx.x >> 5];
-    if (lo1 + lane <= hi1) ws[lane] = p.wx[lo1 + lane - 1];
-    if (lo2 + lane <= hi2) ws[TB + lane] = p.wx[lo2 + lane - 1];
-    __syncwarp();
-    if (m > S) return;
-    const int64_t pitch = p.pitch;
-    const int tl = t0 + jh;  // first column of this lane
-    double acc[SB][PH];
-#pragma unroll
-    for (int i = 0; i < SB; i++)
-#pragma unroll
-        for (int j = 0; j < PH; j++) {
-            const int s = s0 + i, t = tl + j;
-            acc[i][j] = (partial && s <= n && t <= n) ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
-        }
-    for (int r = 0; r < 2; r++) {
-        const int lo = r ? lo2 : lo1, hi = r ? hi2 : hi1;
-        const bool fA = r ? fA2 : fA1, fC = r ? fC2 : fC1;
-        if (hi < lo) continue;
-        // two splits per iteration: all their operand loads are issued before the
-        // arithmetic.  A skipped split (m < w: every cell it feeds is gated,
-        // m < w <= m_null) contributes +inf.
-        for (int sp = lo; sp <= hi; sp += 2) {
-            double a[2][SB], c[2][PH];
-#pragma unroll
-            for (int u = 0; u < 2; u++) {
-                const int q = sp + u;
-                const int w = q <= hi ? ws[r * TB + (q - lo)] : 0;
-                const bool use = q <= hi && m >= w;
-                const double *ap = p.A + a_index(s0, q - 1) * pitch + m;           // A(s0+i, q-1)
-                const double *cp = p.C + cell_index(n, q, tl) * pitch + (m - w);  // C(q, tl+j)
-#pragma unroll
-                for (int i = 0; i < SB; i++) a[u][i] = (use && s0 + i <= n) ? ld(ap + i * pitch, fA) : INFINITY;
-#pragma unroll
-                for (int j = 0; j < PH; j++) c[u][j] = (use && tl + j <= n) ? ld(cp + j * pitch, fC) : INFINITY;
-            }
-#pragma unroll
-            for (int u = 0; u < 2; u++)
-#pragma unroll
-                for (int i = 0; i < SB; i++)
-#pragma unroll
-                    for (int j = 0; j < PH; j++) acc[i][j] = dmin(acc[i][j], __dadd_rn(a[u][i], c[u][j]));
-        }
-    }
-    if (m > S) return;
-#pragma unroll
-    for (int i = 0; i < SB; i++)
-#pragma unroll
-        for (int j = 0; j < PH; j++) {
-            const int s = s0 + i, t = tl + j;
-            if (s <= n && t <= n) p.C[cell_index(n, s, t) * pitch + m] = acc[i][j];
-        }
-}
+constexpr int PH = SB / 2;  // columns per product lane
 
 // The same product with the operands staged through a per-warp shared-memory
 // ring by cp.async (PNS splits in flight per warp, no operand registers held
@@ -201,14 +103,26 @@ __global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product_async(Problem
         hi2 = t0 - 1;
         partial = delta >= 2;
     }
-    const int n1 = max(0, hi1 - lo1 + 1), n2 = max(0, hi2 - lo2 + 1), nsp = n1 + n2;
-    if (nsp == 0 || s0 > n || t0 > n) return;  // uniform over the warp
+    // the middle's fired splits for this sub-tile and 32-m chunk (delta >= 2)
+    const uint16_t *lst = nullptr;
+    int n3 = 0;
+    bool mid_partial = false;  // the middle overflowed its list and wrote the exact partial itself
+    if (partial) {
+        lst = p.mlist + mlist_index(n_mc32(S), I, (item % n_mg) * 16 / 32, alpha * NSB + gamma);
+        const int h = lst[0];
+        mid_partial = h == MLIST_OVERFLOW;
+        n3 = mid_partial ? 0 : h;
+    }
+    const int n1 = max(0, hi1 - lo1 + 1), n2 = max(0, hi2 - lo2 + 1), nsp = n1 + n2 + n3;
+    if (s0 > n || t0 > n) return;      // no cells (uniform over the warp)
+    if (nsp == 0 && (!partial || mid_partial)) return;  // nothing to add; the partial (if any) is final
     int *ws = wxs[wid];
     if (lane < n1) ws[lane] = p.wx[lo1 + lane - 1];
     if (lane < n2) ws[TB + lane] = p.wx[lo2 + lane - 1];
     __syncwarp();
     const int64_t pitch = p.pitch;
     const bool mlive = m <= S;
+    const int sp_mid = i0 + TB;  // s' of middle split index 0
     // split idx: 0..n1-1 -> s' = lo1 + idx (left), n1.. -> s' = lo2 + idx - n1 (right).
     // Issued in order, so the lane walks its operand rows incrementally: rows
     // s0+jh.. of A column q-1 and cells (q, t0+jh..) are consecutive table rows,
@@ -221,11 +135,25 @@ __global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product_async(Problem
         rows_a |= (s0 + jh + i <= n) << i;
         rows_c |= (t0 + jh + i <= n) << i;
     }
-    int nx = 0, q = n1 > 0 ? lo1 : lo2;
+    int nx = 0, q = n1 > 0 ? lo1 : (n2 > 0 ? lo2 : sp_mid);
     const double *pa = p.A + a_index(s0 + jh, q - 1) * pitch + m;
     const double *pc = p.C + cell_index(n, q, t0 + jh) * pitch + m;
     auto issue_next = [&]() {
         double(*st)[SB][16] = ring[wid][nx % PNS];
+        if (nx >= n1 + n2) {  // a split the middle recorded: addresses computed directly
+            const int sp = sp_mid + lst[1 + nx - n1 - n2];
+            const int w = p.wx[sp - 1];
+            const bool use = mlive && m >= w;
+            const double *la = p.A + a_index(s0 + jh, sp - 1) * pitch + m;
+            const double *lc = p.C + cell_index(n, sp, t0 + jh) * pitch + (use ? m - w : m);
+#pragma unroll
+            for (int i = 0; i < PH; i++) {
+                cp_async8_zfill(&st[0][jh + i][mi], la + pitch4[i], use && ((rows_a >> i) & 1));
+                cp_async8_zfill(&st[1][jh + i][mi], lc + pitch4[i], use && ((rows_c >> i) & 1));
+            }
+            ++nx;
+            return;
+        }
         const int w = nx < n1 ? ws[nx] : ws[TB + nx - n1];
         // A skipped operand is zero-filled: m < w means every cell the split
         // feeds is gated (m < w <= m_null, DESIGN Q6), so its partial is never
@@ -257,8 +185,8 @@ __global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product_async(Problem
         for (int i = 0; i < SB; i++) {
 #pragma unroll
             for (int j = 0; j < PH; j++)
-                acc[i][j] = (partial && mlive && s0 + i <= n && ((rows_c >> j) & 1)) ? __ldcg(cr + pitch4[j])
-                                                                                       : INFINITY;
+                acc[i][j] = (mid_partial && mlive && s0 + i <= n && ((rows_c >> j) & 1)) ? __ldcg(cr + pitch4[j])
+                                                                                           : INFINITY;
             cr += (int64_t)(n - (s0 + i)) * pitch;
         }
     }
@@ -696,8 +624,8 @@ inline int leaf_variant() {
 }
 
 // Product kernel: ROTOR_PROD=2 k_sub_product_async at 3 CTAs/SM (default:
-// 222.4 ms per config-4 solve), 1 the same at 4 CTAs/SM (223.2), 3 / 4
-// k_sub_product (operands through registers) at 3 / 4 CTAs/SM (231.4).
+// 222.4 ms per config-4 solve), 1 the same at 4 CTAs/SM (223.2); a variant
+// with the operands through registers (231.4) was removed.
 constexpr int PRODUCT_MINB_DEFAULT = 2;
 inline int product_minb() {
     static const int v = [] {
@@ -727,6 +655,8 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
         bool has_product;
         if (delta == 0) {
             has_product = e >= 2;
+        } else if (delta >= 2) {
+            has_product = true;  // every sub-tile: at least the middle's recorded splits (mlist)
         } else {
             int a, g;
             sub_at(delta, e, 0, a, g);
@@ -735,12 +665,8 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
         if (has_product) {
             if (product_minb() == 1)
                 k_sub_product_async<4><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
-            else if (product_minb() == 2)
-                k_sub_product_async<3><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
-            else if (product_minb() == 4)
-                k_sub_product<4><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
             else
-                k_sub_product<3><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
+                k_sub_product_async<3><<<blocks, DEP_THREADS, 0, st>>>(p, delta, e, tile_lo, ntiles);
             launches++;
         }
         const int lb = ntiles * cnt * n_chunks;

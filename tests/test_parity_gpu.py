@@ -201,8 +201,6 @@ VARIANTS = {
     "leaf_row": {"ROTOR_LEAF": "row"},  # k_sub_leaf<false>: scalars from global memory
     "leaf_tab": {"ROTOR_LEAF": "tab"},  # k_sub_leaf_row<false>: right-range operands not staged
     "prod4": {"ROTOR_PROD": "1"},  # k_sub_product_async at 4 CTAs/SM
-    "prod_reg3": {"ROTOR_PROD": "3"},  # k_sub_product (operands through registers), 3 CTAs/SM
-    "prod_reg4": {"ROTOR_PROD": "4"},
 }
 
 
