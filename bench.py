@@ -203,9 +203,9 @@ def middle_alg_bytes(L: int, S: int, TB: int = 32) -> int:
     """Bytes the middle kernel must move per solve (DESIGN 5.2): for every tile
     (I, J), J - I >= 2, split s' of its middle range and m, the fp32 shadow
     operands A32(s, s'-1, m) of its real rows s and C32(s', t, m - w) of its
-    real columns t are read once (4 B each), and every real cell's partial
-    minimum is written once (8 B) — the operand reuse a tile allows, nothing
-    re-read."""
+    real columns t are read once (4 B each) — the operand reuse a tile allows,
+    nothing re-read.  It writes no partial minima (its fired splits go to the
+    sub-product as lists of <= 32 uint16 per warp and 32 m, < 0.1% of this)."""
     n = L + 1
     nb = (n + TB - 1) // TB
     tot = 0
@@ -213,7 +213,7 @@ def middle_alg_bytes(L: int, S: int, TB: int = 32) -> int:
         cs = min(n, TB * (I + 1)) - TB * I
         for J in range(I + 2, nb):
             ct = min(n, TB * (J + 1)) - TB * J
-            tot += 4 * (cs + ct) * (J - I - 1) * TB + 8 * cs * ct
+            tot += 4 * (cs + ct) * (J - I - 1) * TB
     return tot * (S + 1)
 
 
@@ -705,15 +705,15 @@ def run_ours(args):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "peak_source": peak_kind,
                     "model": "middle_fp32_operand_bytes: the dominant kernel (pruned middle) against HBM on the "
-                             "bytes its tiling cannot avoid (fp32 shadow operands of every tile, split and m once, "
-                             "one 8-byte partial write per cell); NOT the wavefront model of SURVEY 8(d)",
+                             "bytes its tiling cannot avoid (fp32 shadow operands of every tile, split and m once); "
+                             "NOT the wavefront model of SURVEY 8(d)",
                     "traffic": traffic,
                     "traffic_over_alg": (traffic / mb_alg) if traffic else None,
                     "traffic_scope": "DRAM read+write bytes of all middle launches of one solve (ncu launch list, "
                                      "profiles/ncu_summary.json tiled_solve)",
                     "alg_bytes_per_step": mb_alg,
-                    "kernel": "k_tile_middle_wide (pruned middle: fp32 shadow boxes, coarse + per-cell lower-bound "
-                              "filter, exact fp64 recompute with atomic min)",
+                    "kernel": "k_tile_middle_wide (pruned middle: fp32 shadow boxes by bulk copy, coarse + per-cell "
+                              "exact lower-bound filter; fired splits handed to the sub-product)",
                     "transitions_per_step": tm, "middle_ms_per_step": mid_avg_ms,
                     "middle_launches_per_step": mid_launches,
                     "middle_time_note": "sum of the middle launches' CUDA-event durations on their streams inside "

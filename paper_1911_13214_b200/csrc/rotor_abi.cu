@@ -455,6 +455,13 @@ int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind
     b.ops_cap = (const int64_t *)(w + o_cap);
     b.counter = (int *)(w + o_ctr);
     b.order = (const int32_t *)(w + o_ord);
+    // ROTOR_BATCH_MC: m-chunk of k_batch's fill order (config 5, ms per sweep:
+    // whole rows 31.6, 16 m 31.8, 32 m 32.7, 64 m 30.8, 128 m 29.2)
+    static const int batch_mc = [] {
+        const char *e = getenv("ROTOR_BATCH_MC");
+        return e ? atoi(e) : 128;
+    }();
+    b.mc = batch_mc;
     rotor::launch_batch(b, n_slots, st);
     CK(cudaGetLastError());
     std::vector<double> h_c(P);
@@ -463,6 +470,13 @@ int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind
     CK(cudaMemcpyAsync(h_c.data(), w + o_cost, P * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_n.data(), w + o_nops, P * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_s.data(), w + o_st, P * 4, cudaMemcpyDeviceToHost, st));
+    // every problem's ops in ONE copy (the device area holds ops_caps[q] slots
+    // per problem), scattered on the host: one D2H instead of one per problem
+    std::vector<rotor_op> h_ops;
+    if (in.ops && total_ops > 0) {
+        h_ops.resize((size_t)total_ops);
+        CK(cudaMemcpyAsync(h_ops.data(), w + o_ops, (size_t)total_ops * sizeof(rotor_op), cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
     int first_err = ROTOR_OK;
     for (int64_t k = 0; k < P; k++) {
@@ -478,11 +492,9 @@ int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind
         if (sq != ROTOR_OK && sq != ROTOR_INFEASIBLE && sq != ROTOR_ETRUNC && !first_err) first_err = sq;
         if (in.ops && h_n[k] > 0 && h_cap[k] > 0) {
             const int64_t cnt = std::min(h_n[k], h_cap[k]);
-            CK(cudaMemcpyAsync(in.ops + in.ops_offsets[q], w + o_ops + h_off[k] * 8, cnt * 8, cudaMemcpyDeviceToHost,
-                               st));
+            memcpy(in.ops + in.ops_offsets[q], h_ops.data() + h_off[k], (size_t)cnt * sizeof(rotor_op));
         }
     }
-    CK(cudaStreamSynchronize(st));
     if (first_err) return fail(first_err, "batched solve: a problem failed with status %d", first_err);
     return ROTOR_OK;
 }

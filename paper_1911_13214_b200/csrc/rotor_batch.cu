@@ -99,12 +99,21 @@ __global__ void __launch_bounds__(512, 4) k_batch(BatchArgs b) {  // 4 resident 
         const int n = p.n, W = b.S + 1;
         for (int idx = threadIdx.x; idx < n * W; idx += blockDim.x) leaf_cell(p, 1 + idx / W, idx % W);
         __syncthreads();
-        for (int d = 1; d <= L; d++) {
-            for (int idx = threadIdx.x; idx < (n - d) * W; idx += blockDim.x) {
-                const int s = 1 + idx / W;
-                wavefront_cell(p, s, s + d, idx % W);
+        // m-chunk-major order (b.mc m at a time, every diagonal of the chunk
+        // before the next chunk): valid because every operand lies at the same m
+        // (prefix C(s, s'-1, m), a shorter diagonal) or at a lower m (suffix and
+        // F_all at m - shift); the chunk's slice of the table stays in L2 while
+        // its diagonals run, instead of the whole table streaming per diagonal
+        const int mc = b.mc > 0 ? b.mc : W;
+        for (int m0 = 0; m0 < W; m0 += mc) {
+            const int wm = min(mc, W - m0);
+            for (int d = 1; d <= L; d++) {
+                for (int idx = threadIdx.x; idx < (n - d) * wm; idx += blockDim.x) {
+                    const int s = 1 + idx / wm;
+                    wavefront_cell(p, s, s + d, m0 + idx % wm);
+                }
+                __syncthreads();
             }
-            __syncthreads();
         }
         reconstruct_cta(p);
     }

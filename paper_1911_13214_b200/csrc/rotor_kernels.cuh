@@ -26,6 +26,7 @@ struct BatchArgs {
     const int64_t *ops_off, *ops_cap;
     int *counter;               // work queue head, zeroed before the launch
     const int32_t *order;       // [n_problems] hand-out order of the queue (longest chains first)
+    int mc;                     // m-chunk of the fill order (0: whole rows, diagonal by diagonal)
 };
 size_t batch_slot_bytes(int L_max, int S);
 void launch_batch(const BatchArgs &b, int n_slots, cudaStream_t st);
