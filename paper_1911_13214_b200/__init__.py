@@ -316,7 +316,7 @@ def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=No
     if with_ops:
         caps = np.repeat(np.array([max_ops(int(ch.L)) for ch in chains], dtype=np.int64), nl)
         offs = np.concatenate([[0], np.cumsum(caps)[:-1]]).astype(np.int64)
-        ops = np.zeros((int(caps.sum()), 2), dtype=np.int32)
+        ops = np.empty((int(caps.sum()), 2), dtype=np.int32)
     P = lambda a, t: a.ctypes.data_as(_P(t)) if a is not None else None
     dv, nd = _devices(devices)
     r = _lib.rotor_solve_batch(arr, P(Ls, _i32), nc, P(lim, _u64), nl, int(slots), _c.byref(o), P(dv, _i32), nd,
@@ -328,7 +328,7 @@ def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=No
         out_ops = []
         for p in range(nc * nl):
             k = int(n_ops.reshape(-1)[p])
-            out_ops.append(ops[offs[p]: offs[p] + max(k, 0)].copy())
+            out_ops.append(ops[offs[p]: offs[p] + max(k, 0)])  # views into one array
     return costs, status, n_ops, out_ops
 
 

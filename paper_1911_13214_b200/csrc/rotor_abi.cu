@@ -351,6 +351,23 @@ struct BatchOut {
     int32_t *status;
 };
 
+// Per-thread pinned host staging (grown, never shrunk) for device-to-host result copies.
+rotor_op *pinned_staging(size_t bytes) {
+    static thread_local void *buf = nullptr;
+    static thread_local size_t cap = 0;
+    if (cap < bytes) {
+        if (buf) cudaFreeHost(buf);
+        buf = nullptr;
+        cap = 0;
+        if (cudaMallocHost(&buf, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        cap = bytes;
+    }
+    return (rotor_op *)buf;
+}
+
 // The problems idx (global index q = chain * n_limits + limit) on the current
 // device: one fused k_batch launch on `st`, results scattered to the caller's
 // arrays at their global indices (distinct workers write disjoint entries).
@@ -415,7 +432,8 @@ int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind
     const size_t o_d = take(h_d.size() * 8), o_u = take(h_u.size() * 8), o_pc = take(P * 4), o_L = take(n_chains * 4),
                  o_lim = take(P * 8), o_off = take(P * 8), o_cap = take(P * 8), o_cost = take(P * 8),
                  o_nops = take(P * 8), o_st = take(P * 4), o_ops = take((size_t)std::max<int64_t>(total_ops, 1) * 8),
-                 o_ctr = take(8), o_ord = take(P * 4), o_pool = take((size_t)n_slots * slot);
+                 o_ctr = take(8), o_ord = take(P * 4), o_pool = take((size_t)n_slots * slot),
+                 o_cmp = take((size_t)std::max<int64_t>(total_ops, 1) * 8);  // compacted ops
     void *wsv = nullptr;
     Lease lease;
     int r = lease_workspace(kind, off, lease, &wsv);
@@ -470,12 +488,32 @@ int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind
     CK(cudaMemcpyAsync(h_c.data(), w + o_cost, P * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_n.data(), w + o_nops, P * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_s.data(), w + o_st, P * 4, cudaMemcpyDeviceToHost, st));
-    // every problem's ops in ONE copy (the device area holds ops_caps[q] slots
-    // per problem), scattered on the host: one D2H instead of one per problem
-    std::vector<rotor_op> h_ops;
-    if (in.ops && total_ops > 0) {
-        h_ops.resize((size_t)total_ops);
-        CK(cudaMemcpyAsync(h_ops.data(), w + o_ops, (size_t)total_ops * sizeof(rotor_op), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    // the ops: compacted on the device (problem k's min(n_k, cap_k) ops after
+    // the previous problems'), ONE copy into pinned staging, then scattered on
+    // the host into the caller's buffer
+    std::vector<int64_t> h_cnt(P, 0), h_dst(P, 0);
+    int64_t n_copy = 0;
+    if (in.ops) {
+        for (int64_t k = 0; k < P; k++) {
+            h_cnt[k] = h_n[k] > 0 ? std::min(h_n[k], h_cap[k]) : 0;
+            h_dst[k] = n_copy;
+            n_copy += h_cnt[k];
+        }
+    }
+    rotor_op *staged = nullptr;
+    if (n_copy > 0) {
+        // reuse the offsets area of the descriptors: o_off (src offsets), o_cap
+        // (counts) and o_nops (destination offsets) are no longer needed
+        CK(cudaMemcpyAsync(w + o_cap, h_cnt.data(), P * 8, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(w + o_nops, h_dst.data(), P * 8, cudaMemcpyHostToDevice, st));
+        rotor_op *dev_dst = (rotor_op *)(w + o_cmp);
+        rotor::launch_compact_ops((const rotor_op *)(w + o_ops), (const int64_t *)(w + o_off),
+                                  (const int64_t *)(w + o_cap), (const int64_t *)(w + o_nops), dev_dst, (int)P, st);
+        CK(cudaGetLastError());
+        staged = pinned_staging((size_t)n_copy * sizeof(rotor_op));
+        if (!staged) return fail(ROTOR_ENOMEM, "pinned staging of %lld ops failed", (long long)n_copy);
+        CK(cudaMemcpyAsync(staged, dev_dst, (size_t)n_copy * sizeof(rotor_op), cudaMemcpyDeviceToHost, st));
     }
     CK(cudaStreamSynchronize(st));
     int first_err = ROTOR_OK;
@@ -490,10 +528,7 @@ int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind
         if (out.n_ops) out.n_ops[q] = (sq == ROTOR_OK || sq == ROTOR_ETRUNC) ? h_n[k] : -1;
         out.costs[q] = sq == ROTOR_INFEASIBLE ? INFINITY : h_c[k];
         if (sq != ROTOR_OK && sq != ROTOR_INFEASIBLE && sq != ROTOR_ETRUNC && !first_err) first_err = sq;
-        if (in.ops && h_n[k] > 0 && h_cap[k] > 0) {
-            const int64_t cnt = std::min(h_n[k], h_cap[k]);
-            memcpy(in.ops + in.ops_offsets[q], h_ops.data() + h_off[k], (size_t)cnt * sizeof(rotor_op));
-        }
+        if (h_cnt[k] > 0) memcpy(in.ops + in.ops_offsets[q], staged + h_dst[k], (size_t)h_cnt[k] * sizeof(rotor_op));
     }
     if (first_err) return fail(first_err, "batched solve: a problem failed with status %d", first_err);
     return ROTOR_OK;

@@ -121,6 +121,22 @@ __global__ void __launch_bounds__(512, 4) k_batch(BatchArgs b) {  // 4 resident 
 
 size_t batch_slot_bytes(int L_max, int S) { return slot_layout(L_max, S).bytes; }
 
+// Gather every problem's ops (src + src_off[k], cnt[k] of them) into one
+// contiguous array (dst + dst_off[k]) for a single device-to-host copy.
+__global__ void k_compact_ops(const rotor_op *src, const int64_t *src_off, const int64_t *cnt, const int64_t *dst_off,
+                              rotor_op *dst, int P) {
+    for (int k = blockIdx.x; k < P; k += gridDim.x) {
+        const rotor_op *a = src + src_off[k];
+        rotor_op *b = dst + dst_off[k];
+        for (int64_t i = threadIdx.x; i < cnt[k]; i += blockDim.x) b[i] = a[i];
+    }
+}
+
+void launch_compact_ops(const rotor_op *src, const int64_t *src_off, const int64_t *cnt, const int64_t *dst_off,
+                        rotor_op *dst, int P, cudaStream_t st) {
+    k_compact_ops<<<P < 1024 ? P : 1024, 128, 0, st>>>(src, src_off, cnt, dst_off, dst, P);
+}
+
 void launch_batch(const BatchArgs &b, int n_slots, cudaStream_t st) { k_batch<<<n_slots, 512, 0, st>>>(b); }
 
 }  // namespace rotor

@@ -30,6 +30,8 @@ struct BatchArgs {
 };
 size_t batch_slot_bytes(int L_max, int S);
 void launch_batch(const BatchArgs &b, int n_slots, cudaStream_t st);
+void launch_compact_ops(const rotor_op *src, const int64_t *src_off, const int64_t *cnt, const int64_t *dst_off,
+                        rotor_op *dst, int P, cudaStream_t st);
 
 // Tiled fill (rotor_fill_tiled.cu). Returns the number of kernels launched (-1: setup error).
 // mid_ev (optional, 2 * mid_cap events): recorded around each middle-kernel launch
