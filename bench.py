@@ -77,11 +77,16 @@ def init_nccl(dist, dev):
     """init_process_group("nccl") with the process's stdout silenced at the fd level
     while the communicator comes up (NCCL writes its version banner there), so
     rank 0's stdout carries only the JSON line."""
+    import datetime
+
+    # NCCL errors / hangs abort the communicator and surface as exceptions
+    os.environ.setdefault("TORCH_NCCL_ASYNC_ERROR_HANDLING", "1")
     sys.stdout.flush()
     saved, null = os.dup(1), os.open(os.devnull, os.O_WRONLY)
     os.dup2(null, 1)
     try:
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group("nccl", device_id=dev,
+                                timeout=datetime.timedelta(seconds=float(os.environ.get("ROTOR_NCCL_TIMEOUT_S", "600"))))
         dist.barrier()
         import torch
 

@@ -16,11 +16,22 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "rotor.h"
 #include "rotor_common.cuh"
 #include "rotor_kernels.cuh"
 
 namespace {
+
+// NVTX ranges around the host-side phases of every entry point (no-ops unless a
+// profiler such as Nsight Systems is attached): a timeline of a solve is
+// segmented into precompute / fill / reconstruct, per tile diagonal and per
+// sharded rank.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 thread_local std::string g_err;
 
@@ -295,8 +306,12 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
         CK(cudaEventRecord(g_last.ev[0], st));
     }
     int launches = 0;
-    rotor::launch_precompute(dch, M, p, st);
-    rotor::launch_leaf(p, st);
+    NvtxRange nv_solve("rotor.solve");
+    {
+        NvtxRange nv("rotor.precompute+leaf");
+        rotor::launch_precompute(dch, M, p, st);
+        rotor::launch_leaf(p, st);
+    }
     launches += 2;
     CK(cudaGetLastError());
     if (o.profile) CK(cudaEventRecord(g_last.ev[1], st));
@@ -313,18 +328,23 @@ int enqueue_solve(const rotor_chain &dch, uint64_t M, const Layout &y, char *ws,
                 g_last.mid_ev.push_back(e);
             }
         }
-        fill = rotor::launch_fill_tiled(p, st, o.schedule, cap ? g_last.mid_ev.data() : nullptr, cap, &g_last.mid_n);
+        {
+            NvtxRange nv("rotor.fill.tiled");
+            fill = rotor::launch_fill_tiled(p, st, o.schedule, cap ? g_last.mid_ev.data() : nullptr, cap, &g_last.mid_n);
+        }
         if (fill < 0) {
             cudaError_t e = cudaGetLastError();
             return fail(ROTOR_EDEVICE, "tiled fill launch failed: %s", cudaGetErrorString(e));
         }
     } else {
+        NvtxRange nv("rotor.fill.wavefront");
         for (int d = 1; d <= y.L; d++) rotor::launch_diag_wavefront(p, d, st);
         fill = y.L;
     }
     CK(cudaGetLastError());
     launches += fill;
     if (o.profile) CK(cudaEventRecord(g_last.ev[2], st));
+    NvtxRange nv_rec("rotor.reconstruct");
     rotor::launch_reconstruct(p, st);
     launches += 1;
     CK(cudaGetLastError());
@@ -373,6 +393,7 @@ rotor_op *pinned_staging(size_t bytes) {
 // arrays at their global indices (distinct workers write disjoint entries).
 int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind, cudaStream_t st,
                     const BatchOut &out) {
+    NvtxRange nv("rotor.batch");
     const int64_t P = (int64_t)idx.size();
     if (P == 0) return ROTOR_OK;
     const int n_chains = in.n_chains, slots = in.slots;
@@ -976,7 +997,11 @@ int sharded_run(const rotor_chain *chain, int L, uint64_t M, int S, const rotor_
         CK(cudaEventRecord(q.ev_copied, q.st));
     }
     std::vector<int> lo, hi;
+    NvtxRange nv_fill("rotor.sharded.fill");
     for (int delta = 0; delta < nb; delta++) {
+        char nm[48];
+        snprintf(nm, sizeof nm, "rotor.sharded.delta=%d", delta);
+        NvtxRange nv_d(nm);
         tile_ranges(nb - delta, R, lo, hi);
         for (int r = 0; r < R; r++) {  // every rank: its share of the tiles of this diagonal
             ShardRank &q = rk[r];

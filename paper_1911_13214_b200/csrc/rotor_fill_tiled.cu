@@ -23,11 +23,14 @@
 #include <cudaTypedefs.h>
 #include <math.h>
 #include <stdlib.h>
+#include <stdio.h>
 #include <string.h>
 #include <limits.h>
 
 #include <map>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "rotor_common.cuh"
 #include "rotor_kernels.cuh"
@@ -872,18 +875,29 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st, int schedule, cudaEvent
     int launches = 0;
     DagRes *r = schedule == 0 ? dag_res(nb) : nullptr;
     if (!r) {
-        for (int delta = 0; delta < nb; delta++) launches += tiled_delta(p, &ctx, delta, 0, nb - delta, st);
+        for (int delta = 0; delta < nb; delta++) {
+            char nm[40];
+            snprintf(nm, sizeof nm, "rotor.fill.delta=%d", delta);
+            nvtxRangePushA(nm);
+            launches += tiled_delta(p, &ctx, delta, 0, nb - delta, st);
+            nvtxRangePop();
+        }
     } else {
         std::vector<int> phase(nb, 0);  // (middle launches are timed on their own streams; they overlap)
         cudaEventRecord(r->start, st);
         for (int I = 0; I < nb; I++) cudaStreamWaitEvent(r->st[I], r->start, 0);
-        for (int delta = 0; delta < nb; delta++)
+        for (int delta = 0; delta < nb; delta++) {
+            char nm[40];
+            snprintf(nm, sizeof nm, "rotor.fill.delta=%d", delta);
+            nvtxRangePushA(nm);  // host enqueue of the tile diagonal's tasks
             for (int I = 0; I + delta < nb; I++) {
                 // (I+1, I+delta) is the latest record of ev[I+1]: row I+1 is enqueued after row I
                 if (delta >= 1) cudaStreamWaitEvent(r->st[I], r->ev[I + 1], 0);
                 launches += tiled_delta_ep(p, &ctx, delta, I, I + 1, r->st[I], phase[I]);
                 cudaEventRecord(r->ev[I], r->st[I]);
             }
+            nvtxRangePop();
+        }
         for (int I = 0; I < nb; I++) cudaStreamWaitEvent(st, r->ev[I], 0);
     }
     if (mid_n) *mid_n = ctx.mid_n;

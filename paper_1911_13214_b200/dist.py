@@ -83,6 +83,34 @@ class CudaShardEngine:
         return int(out["status"].item()), float(out["cost"].item()), out["ops"][: max(k, 0)].cpu().numpy()
 
 
+def _collective_timeout():
+    """Seconds a per-diagonal collective may take (ROTOR_COLLECTIVE_TIMEOUT_S, default 300)."""
+    import os
+
+    return float(os.environ.get("ROTOR_COLLECTIVE_TIMEOUT_S", "300"))
+
+
+class CollectiveError(RuntimeError):
+    """A per-diagonal exchange failed or timed out (a rank died, NCCL error, hang)."""
+
+
+def _all_gather_checked(recv, send, group, delta):
+    """all_gather_into_tensor as an async op, waited with a timeout: a failed or
+    hung peer surfaces as CollectiveError naming the tile diagonal instead of a
+    silent hang (NCCL's own async error handling aborts the communicator)."""
+    import datetime
+
+    import torch.distributed as dist
+
+    work = dist.all_gather_into_tensor(recv, send, group=group, async_op=True)
+    try:
+        ok = work.wait(timeout=datetime.timedelta(seconds=_collective_timeout()))
+    except Exception as e:  # NCCL / gloo error reported by the backend
+        raise CollectiveError(f"all-gather of tile diagonal {delta} failed: {e}") from e
+    if ok is False:
+        raise CollectiveError(f"all-gather of tile diagonal {delta} timed out after {_collective_timeout()} s")
+
+
 def solve_sharded(engine, group=None):
     """one table sharded over the ranks of `group`.
 
@@ -108,7 +136,7 @@ def solve_sharded(engine, group=None):
         send = engine.buffer("send", cap)
         engine.pack(delta, lo, hi, send)
         recv = engine.buffer("recv", cap * world)
-        dist.all_gather_into_tensor(recv, send, group=group)
+        _all_gather_checked(recv, send, group, delta)
         for r, (l, h) in enumerate(ranges):
             if r != rank and h > l:
                 engine.unpack(delta, l, h, recv[r * cap * tb: (r * cap + (h - l)) * tb])

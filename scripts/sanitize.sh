@@ -11,19 +11,26 @@ import sys
 sys.path.insert(0, ".")
 import chaingen as G
 import paper_1911_13214_b200 as R
+import os
 rng = G.SplitMix64(3)
-for L, S in [(70, 45), (33, 20)]:
+# L = 230 (8 tile blocks: middle launches up to delta = 7, every leaf / product
+# phase), S = 520 (17 m-chunks of the middle, 5 leaf chunks), both schedules
+for L, S in [(230, 520), (70, 45), (33, 20)]:
     ch = G.random_chain(rng, L, real_times=True, big=True)
     M = int(sum(int(x) for x in ch.wbx) * 0.25)
-    for k in ("tiled", "wavefront"):
-        r = R.solve(ch, M, S, kernel=k)
-        print(k, L, S, r.status, r.cost, r.n_ops)
+    for k, sch in (("tiled", "dag"), ("tiled", "diagonal"), ("wavefront", "dag")):
+        if L > 100 and k == "wavefront" and os.environ.get("SAN_FAST"):
+            continue
+        r = R.solve(ch, M, S, kernel=k, schedule=sch)
+        print(k, sch, L, S, r.status, r.cost, r.n_ops)
     R.export_tables(L + 1, S)
+r = R.solve_sharded(ch, M, S, [0, 0], halo_mode=1)
+print("sharded", r.status, r.cost)
 chains, limits, S = G.config5(n_limits=3)
 costs, status, n_ops, ops = R.solve_batch(chains[:3], [l[:3] for l in limits[:3]], 60, with_ops=True)
 print("batch", costs.shape, status.tolist())
 EOF
 for tool in ${TOOLS:-memcheck racecheck synccheck initcheck}; do
-  timeout 900 compute-sanitizer --tool $tool --print-limit 200 python /tmp/san_run.py > "$OUT/$tool.log" 2>&1
+  timeout 1500 compute-sanitizer --tool $tool --print-limit 200 python /tmp/san_run.py > "$OUT/$tool.log" 2>&1
   echo "$tool rc=$? $(grep -E 'ERROR SUMMARY|RACECHECK SUMMARY' "$OUT/$tool.log" | tail -1)"
 done

@@ -177,3 +177,46 @@ def test_sharded_virtual_ranks_gpu(world, oracle_mod):
             assert np.array_equal(C.view(np.uint64), Co.view(np.uint64))
         del engines
         torch.cuda.empty_cache()
+
+
+def _worker_stall(rank, world, port, q):
+    """Rank 1 never joins the exchange: rank 0 must fail with CollectiveError
+    naming the tile diagonal within ROTOR_COLLECTIVE_TIMEOUT_S, not hang."""
+    import datetime
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    os.environ["ROTOR_COLLECTIVE_TIMEOUT_S"] = "3"
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=20))
+    try:
+        if rank == 1:
+            q.put((rank, "idle"))
+            return
+        import oracle as O
+        from paper_1911_13214_b200.dist import CollectiveError, solve_sharded
+
+        ch, M, S = _reference()
+        ref, _ = O.OracleSolve(ch, M, S).tables()
+        try:
+            solve_sharded(FakeEngine(ref, ch.L + 1, S))
+            q.put((rank, "no error"))
+        except CollectiveError as e:
+            q.put((rank, "CollectiveError: " + str(e)))
+    except Exception as e:
+        q.put((rank, repr(e)))
+
+
+def test_sharded_exchange_timeout_gloo():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker_stall, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = dict(q.get(timeout=120) for _ in range(2))
+    for p in ps:
+        p.join(timeout=30)
+        if p.is_alive():
+            p.kill()
+    assert out[1] == "idle"
+    assert out[0].startswith("CollectiveError") and "tile diagonal" in out[0], out[0]
