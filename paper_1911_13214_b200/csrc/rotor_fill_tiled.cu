@@ -474,7 +474,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NWARPS);
+            mbar_init(&empty[s], CONSUMERS);
             claim[s] = s;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -606,17 +606,20 @@ __global__ void __launch_bounds__(THREADS, 1)
                 }
             }
             nf += __popc(needk);
-            // Release stage st (mbarrier arrive: release of this warp's reads); the
+            // Release stage st (mbarrier arrive: release of the thread's reads); the
             // warp whose arrival completes the phase sees it with a non-blocking
             // test (acquire) and refills the stage at once — no warp ever blocks
             // on slower ones (a dedicated producer warp would not fit the register
             // file).  The CAS hands the refill to exactly one warp.
-            __syncwarp();
+            // (every thread arrives — count CONSUMERS — rather than lane 0 after a
+            // __syncwarp: the same cost here, and compute-sanitizer's racecheck
+            // then sees each thread's own release of its reads)
+            mbar_arrive(&empty[st]);
             if (lane == 0) {
-                mbar_arrive(&empty[st]);
                 if (gi + STAGES < total && mbar_test(&empty[st], (uint32_t)((gi / STAGES) & 1)) &&
-                    atomicCAS(&claim[st], gi, gi + STAGES) == gi)
+                    atomicCAS(&claim[st], gi, gi + STAGES) == gi) {
                     issue(gi + STAGES);
+                }
             }
         }
         __syncwarp();

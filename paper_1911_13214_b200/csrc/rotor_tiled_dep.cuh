@@ -437,6 +437,9 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
 
 // Off-diagonal leaf row r at one m (thread = m), scalars from the table; the
 // same arithmetic as leaf_row<false>.
+// r: the row index as a compile-time constant (every loop trimmed and fully
+// unrolled: 8 row bodies, ~26 KB of SASS each; one runtime-row body, 3.6x less
+// code, measured slower in the tile-DAG schedule too: 143.2 vs 131.1 ms per solve)
 template <int r, bool RS, class Wait>
 __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T, bool fresh, bool partial, int s0,
                                              int t0, int m, bool live, const double *Rs, Wait wait) {
@@ -618,6 +621,7 @@ inline int leaf_variant() {
         if (!e) return (int)LEAF_VARIANT_DEFAULT;
         if (!strcmp(e, "tab")) return (int)LEAF_VARIANT_TAB;
         if (!strcmp(e, "tabr")) return (int)LEAF_VARIANT_TABR;
+
         return (int)LEAF_VARIANT_ROW;
     }();
     return v;
@@ -676,6 +680,7 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
             k_sub_leaf_row<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         else if (leaf_variant() == LEAF_VARIANT_TABR)
             k_sub_leaf_row<true><<<lb, LEAF_M, NPAIR * LEAF_M * 8, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
+
         else
             k_sub_leaf<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
         launches++;
