@@ -677,6 +677,7 @@ def run_ours(args):
             "dependent_exact": c["dependent_nominal"],
             "middle_warp_cycles": {k: c[f"middle_{k}_cycles"] for k in ("wait", "init", "loop", "flush")},
             "middle_warp_imbalance": c["middle_warp_imbalance"],
+            "middle_slot_cycles": c["middle_slot_cycles"],
             "note": "value counts NOMINAL transitions (every cell of diagonal d: d + 1 candidates, Eq. 2); "
                     "evaluated = fp32 filter compares + fp64 exact candidates of the pruned middle + every "
                     "candidate of the dependent phase; the middle skips the rest by exact lower bounds "

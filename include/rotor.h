@@ -304,6 +304,7 @@ typedef struct {
     uint64_t middle_loop_cycles;    /* the filter over the splits */
     uint64_t middle_flush_cycles;   /* the exact fp64 pass of the fired splits */
     double middle_warp_imbalance;   /* max / mean over the 16 warp slots of (loop + flush) cycles */
+    uint64_t middle_slot_cycles[16];/* (loop + flush) cycles per warp slot = 8 x 8 sub-tile position in the tile */
 } rotor_counters;
 int rotor_last_counters(rotor_counters *out);
 

@@ -67,7 +67,7 @@ class rotor_counters(ctypes.Structure):
         ("quadrant_compares", ctypes.c_uint64), ("exact_splits", ctypes.c_uint64), ("evaluated", ctypes.c_double),
         ("middle_wait_cycles", ctypes.c_uint64), ("middle_init_cycles", ctypes.c_uint64),
         ("middle_loop_cycles", ctypes.c_uint64), ("middle_flush_cycles", ctypes.c_uint64),
-        ("middle_warp_imbalance", ctypes.c_double),
+        ("middle_warp_imbalance", ctypes.c_double), ("middle_slot_cycles", ctypes.c_uint64 * 16),
     ]
 
 
@@ -282,7 +282,9 @@ def last_counters() -> dict:
     """Work counters of the last solve (options counters=True; include/rotor.h rotor_counters)."""
     c = rotor_counters()
     _check(_lib.rotor_last_counters(_c.byref(c)))
-    return {k: getattr(c, k) for k, _ in rotor_counters._fields_}
+    out = {k: getattr(c, k) for k, _ in rotor_counters._fields_}
+    out["middle_slot_cycles"] = list(c.middle_slot_cycles)
+    return out
 
 
 def _devices(devices):

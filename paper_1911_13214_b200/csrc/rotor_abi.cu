@@ -1232,6 +1232,7 @@ int rotor_last_counters(rotor_counters *out) {
     for (int w = 0; w < 16; w++) {
         mx = std::max(mx, c[8 + w]);
         sum += c[8 + w];
+        out->middle_slot_cycles[w] = c[8 + w];
     }
     out->middle_warp_imbalance = sum ? mx * 16.0 / (double)sum : 0.0;
     return ROTOR_OK;

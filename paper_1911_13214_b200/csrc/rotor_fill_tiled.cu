@@ -394,7 +394,8 @@ struct WideRing {
     static constexpr int KC = KC_, STAGES = STAGES_;
     static constexpr int ST = 2 * KC * BOX;  // floats per stage: KC A boxes, then KC C boxes
     // + the fired-split lists: NWARPS x fmax uint16 (wide_list_bytes)
-    static constexpr size_t bytes = (size_t)STAGES * ST * 4 + 2 * STAGES * 8 + STAGES * 4 + 64;
+    static constexpr size_t bytes =
+        (size_t)STAGES * ST * 4 + 2 * STAGES * 8 + (size_t)STAGES * 2 * KC * 8 + 2 * STAGES * 4 + 64;
 };
 // fired-split list length per warp: every split of the longest item
 // ((nb - 2) * TB), capped by FMAX_CAP and by the shared memory left next to
@@ -433,8 +434,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     float *ring = fsm;  // [STAGES][A: KC][TB s][TMW] [C: KC][TB t][TMW]
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + STAGES * ST);
     uint64_t *empty = full + STAGES;
-    int *claim = reinterpret_cast<int *>(empty + STAGES);  // step whose refill of the stage is still unclaimed
-    int *wx_s = claim + STAGES;                            // wx[0..n) when n <= WIDE_WX_MAX
+    const float **src = reinterpret_cast<const float **>(empty + STAGES);  // [STAGES][2 KC] next refill's boxes
+    int *claim = reinterpret_cast<int *>(src + STAGES * 2 * KC);  // step whose refill of the stage is unclaimed
+    int *prep = claim + STAGES;                                   // step whose refill addresses are not yet computed
+    int *wx_s = prep + STAGES;                                    // wx[0..n) when n <= WIDE_WX_MAX
     uint16_t *fl_s = reinterpret_cast<uint16_t *>(wx_s + (n_wx_smem(p.n) ? p.n : 0));  // [NWARPS][fmax]
 
     const int n = p.n;
@@ -471,11 +474,32 @@ __global__ void __launch_bounds__(THREADS, 1)
             bulk_load(dst + (KC + k) * BOX, p.C32 + shadow_index(p.srows, cell_index(n, sp0 + k, j0), m0), BOX * 4,
                       &full[st]);
     };
+    // Refills are split in two: the FIRST warp to finish reading a stage
+    // computes the source addresses of its next refill (one box per lane,
+    // lane < 2 KC) into shared memory; the LAST one issues the copies from
+    // them.  The last arriver is the slowest warp; with the whole refill on it
+    // (coordinates, 64-bit address arithmetic, copies) it had stayed the
+    // slowest for good (the issuing warp at ~1.23x the others' loop cycles).
+    auto prepare_warp = [&](int gi, int ln) {  // addresses of step gi's boxes
+        int i0, j0, m0, sp0;
+        coords(gi, i0, j0, m0, sp0);
+        if (ln < KC)
+            src[(gi % STAGES) * 2 * KC + ln] = p.A32 + shadow_index(p.srows, a_index(i0, sp0 + ln - 1), m0);
+        else if (ln < 2 * KC)
+            src[(gi % STAGES) * 2 * KC + ln] = p.C32 + shadow_index(p.srows, cell_index(n, sp0 + ln - KC, j0), m0);
+    };
+    auto issue_warp = [&](int gi, int ln) {  // lane 0 posts the expected bytes first
+        const int st = gi % STAGES;
+        if (ln == 0) mbar_expect_tx(&full[st], (uint32_t)(ST * 4));
+        __syncwarp();
+        if (ln < 2 * KC) bulk_load(ring + st * ST + ln * BOX, src[st * 2 * KC + ln], BOX * 4, &full[st]);
+    };
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], CONSUMERS);
             claim[s] = s;
+            prep[s] = s;
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -614,13 +638,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             // (every thread arrives — count CONSUMERS — rather than lane 0 after a
             // __syncwarp: the same cost here, and compute-sanitizer's racecheck
             // then sees each thread's own release of its reads)
-            mbar_arrive(&empty[st]);
-            if (lane == 0) {
-                if (gi + STAGES < total && mbar_test(&empty[st], (uint32_t)((gi / STAGES) & 1)) &&
-                    atomicCAS(&claim[st], gi, gi + STAGES) == gi) {
-                    issue(gi + STAGES);
-                }
-            }
+            int first = 0;  // the first warp done with stage st prepares its next refill
+            if (lane == 0) first = gi + STAGES < total && atomicCAS(&prep[st], gi, gi + STAGES) == gi;
+            if (__shfl_sync(0xffffffffu, first, 0)) prepare_warp(gi + STAGES, lane);
+            mbar_arrive(&empty[st]);  // (after the addresses: the arrive releases them too)
+            int claimed = 0;
+            if (lane == 0)
+                claimed = gi + STAGES < total && mbar_test(&empty[st], (uint32_t)((gi / STAGES) & 1)) &&
+                          atomicCAS(&claim[st], gi, gi + STAGES) == gi;
+            if (__shfl_sync(0xffffffffu, claimed, 0)) issue_warp(gi + STAGES, lane);
         }
         __syncwarp();
         lap(c_loop);
