@@ -98,6 +98,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// (x0 + y0, x1 + y1) rounded toward -inf, as one packed FADD2.RM (sm_100)
+__device__ __forceinline__ float2 fadd2_rd(float2 x, float2 y) {
+    unsigned long long r;
+    asm("add.rm.f32x2 %0, %1, %2;"
+        : "=l"(r)
+        : "l"(*reinterpret_cast<unsigned long long *>(&x)), "l"(*reinterpret_cast<unsigned long long *>(&y)));
+    return *reinterpret_cast<float2 *>(&r);
+}
+
 // non-blocking: true once the phase with this parity has completed (acquire)
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
     uint32_t ok;
@@ -588,11 +597,14 @@ __global__ void __launch_bounds__(THREADS, 1)
                             const bool maybe = !coarse || __fadd_rd(ma[qa], mb[qb]) < maxq[qa][qb];
                             if (__any_sync(0xffffffffu, maybe)) {
                                 if (COUNT) c_quads++;
+                                // two cells per packed FADD2.RM (the same rounding per element)
 #pragma unroll
                                 for (int i = 4 * qa; i < 4 * qa + 4; i++)
 #pragma unroll
-                                    for (int j = 4 * qb; j < 4 * qb + 4; j++)
-                                        nk |= __fadd_rd(a[i], b[j]) < bestf[i][j];
+                                    for (int j = 4 * qb; j < 4 * qb + 4; j += 2) {
+                                        const float2 lb = fadd2_rd(make_float2(a[i], a[i]), make_float2(b[j], b[j + 1]));
+                                        nk |= (lb.x < bestf[i][j]) | (lb.y < bestf[i][j + 1]);
+                                    }
                             }
                         }
                 }
@@ -861,6 +873,7 @@ struct DagRes {
     std::vector<cudaEvent_t> ev;
     cudaEvent_t start = nullptr;
 };
+constexpr int DAG_MAX_STREAMS = 64;  // rows share streams beyond this (long chains: nb > 64)
 DagRes *dag_res(int nb) {
     static thread_local std::map<int, DagRes> res;
     int dev = 0;
@@ -870,15 +883,18 @@ DagRes *dag_res(int nb) {
     static const int prio = env_int("ROTOR_DAG_PRIO", 1);  // rows with lower I first (127.4 vs 129.1 ms per solve; 0: all equal)
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
-    while ((int)r.st.size() < nb) {
+    const int ns = min(nb, DAG_MAX_STREAMS);
+    while ((int)r.st.size() < ns) {
         cudaStream_t s;
-        cudaEvent_t e;
         const int i = (int)r.st.size();
         // priority levels spread over the rows: row 0 the highest
-        const int pr = prio ? greatest + (least - greatest) * i / max(1, nb - 1) : least;
+        const int pr = prio ? greatest + (least - greatest) * i / max(1, ns - 1) : least;
         if (cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, pr) != cudaSuccess) return nullptr;
-        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
         r.st.push_back(s);
+    }
+    while ((int)r.ev.size() < nb) {  // one event per tile row
+        cudaEvent_t e;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
         r.ev.push_back(e);
     }
     return &r;
@@ -913,21 +929,25 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st, int schedule, cudaEvent
         }
     } else {
         std::vector<int> phase(nb, 0);  // (middle launches are timed on their own streams; they overlap)
+        // row I on stream I mod ns: rows sharing a stream only add order between
+        // tasks that are enqueued in dependency order anyway (diagonal-major)
+        const int ns = (int)r->st.size();
+        auto row_st = [&](int I) { return r->st[I % ns]; };
         cudaEventRecord(r->start, st);
-        for (int I = 0; I < nb; I++) cudaStreamWaitEvent(r->st[I], r->start, 0);
+        for (int k = 0; k < ns; k++) cudaStreamWaitEvent(r->st[k], r->start, 0);
         for (int delta = 0; delta < nb; delta++) {
             char nm[40];
             snprintf(nm, sizeof nm, "rotor.fill.delta=%d", delta);
             nvtxRangePushA(nm);  // host enqueue of the tile diagonal's tasks
             for (int I = 0; I + delta < nb; I++) {
                 // (I+1, I+delta) is the latest record of ev[I+1]: row I+1 is enqueued after row I
-                if (delta >= 1) cudaStreamWaitEvent(r->st[I], r->ev[I + 1], 0);
-                launches += tiled_delta_ep(p, &ctx, delta, I, I + 1, r->st[I], phase[I]);
-                cudaEventRecord(r->ev[I], r->st[I]);
+                if (delta >= 1) cudaStreamWaitEvent(row_st(I), r->ev[I + 1], 0);
+                launches += tiled_delta_ep(p, &ctx, delta, I, I + 1, row_st(I), phase[I]);
+                cudaEventRecord(r->ev[I], row_st(I));
             }
             nvtxRangePop();
         }
-        for (int I = 0; I < nb; I++) cudaStreamWaitEvent(st, r->ev[I], 0);
+        for (int I = 0; I < nb; I++) cudaStreamWaitEvent(st, r->ev[I], 0);  // (I < ns covers every stream)
     }
     if (mid_n) *mid_n = ctx.mid_n;
     return launches;

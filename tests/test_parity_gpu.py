@@ -521,3 +521,34 @@ def test_tiled_schedules(R, oracle_mod, schedule):
         C, _ = R.export_tables(ch.L + 1, p.slots, D=False)
         assert_tables_equal(C, o.table_view(), f"{schedule} {p.name}")
         assert res.cost == o.cost and res.op_list() == (o.reconstruct() or [])
+
+
+def test_dag_shared_streams_long_chain(R, oracle_mod):
+    """A chain long enough for more tile rows than DAG streams (L = 2100: 66 tile
+    rows on 64 streams, rows sharing a stream): the DAG schedule's full table
+    equals the diagonal schedule's bit for bit, and both equal the oracle on
+    windows at both ends of the chain and on the top cost / schedule replay."""
+    O = oracle_mod
+    rng = G.SplitMix64(2100)
+    ch = G.random_chain(rng, 2100, real_times=True, big=True)
+    S = 30
+    M = max(1, int(sum(int(x) for x in ch.wbx) * 0.05))
+    n = ch.L + 1
+    r1 = R.solve(ch, M, S, kernel="tiled", schedule="dag")
+    C1, _ = R.export_tables(n, S, D=False)
+    r2 = R.solve(ch, M, S, kernel="tiled", schedule="diagonal")
+    C2, _ = R.export_tables(n, S, D=False)
+    assert_tables_equal(C1, C2, "dag vs diagonal, L=2100")
+    assert r1.cost == r2.cost and r1.op_list() == r2.op_list()
+    for (s0, t0) in [(1, 70), (2040, n)]:
+        o = O.OracleSolve(ch, M, S, window=(s0, t0), threads=O.max_threads(), keep_d=False)
+        cells = _window_cells(s0, t0)
+        nw = t0 - s0 + 1
+        Co = o.table_view()
+        got = np.stack([C1[O.cell_index(n, s, t)] for s, t in cells])
+        want = np.stack([Co[O.cell_index(nw, s - s0 + 1, t - s0 + 1)] for s, t in cells])
+        assert_tables_equal(got, want, f"L=2100 window {s0}..{t0}")
+    if r1.status == R.OK:
+        sz = O.OracleSolve(ch, M, S, fill=False).sizes()
+        rep = O.simulate(r1.op_list(), sz, S)
+        assert rep.valid and abs(rep.makespan - r1.cost) <= r1.n_ops * math.ulp(r1.cost)
