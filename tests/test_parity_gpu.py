@@ -552,3 +552,31 @@ def test_dag_shared_streams_long_chain(R, oracle_mod):
         sz = O.OracleSolve(ch, M, S, fill=False).sizes()
         rep = O.simulate(r1.op_list(), sz, S)
         assert rep.valid and abs(rep.makespan - r1.cost) <= r1.n_ops * math.ulp(r1.cost)
+
+
+@pytest.mark.parametrize("restricted", [False, True])
+def test_config5_all_costs_vs_oracle(R, oracle_mod, restricted):
+    """The whole config-5 sweep (8 chains x 256 limits = 2048 tables, S=500) in one
+    fused launch: EVERY cost bit-equal to the oracle's (all-core OpenMP fill,
+    bit-identical to one thread), in both modes (restricted = the paper's
+    revolve baseline, used by strategies.compare); statuses agree
+    (infeasible exactly where the oracle's cost is +inf); a sample of schedules
+    equals the oracle's Algorithm 2."""
+    O = oracle_mod
+    chains, limits, S = G.config5()
+    costs, status, n_ops, ops = R.solve_batch(chains, limits, S, with_ops=True, restricted=restricted)
+    nl = len(limits[0])
+    thr = O.max_threads()
+    rng = G.SplitMix64(55 + restricted)
+    sample = {(rng.randint(0, len(chains) - 1), rng.randint(0, nl - 1)) for _ in range(24)}
+    for i, ch in enumerate(chains):
+        for j in range(nl):
+            o = O.OracleSolve(ch, limits[i][j], S, restricted=restricted, threads=thr, keep_d=False)
+            c = o.cost
+            if math.isinf(c):
+                assert status[i, j] == R.INFEASIBLE and math.isinf(costs[i, j]), (i, j)
+            else:
+                assert status[i, j] == R.OK, (i, j, status[i, j])
+                assert bits(np.array([costs[i, j]])) == bits(np.array([c])), (i, j, costs[i, j], c)
+                if (i, j) in sample:
+                    assert [tuple(map(int, r)) for r in ops[i * nl + j]] == o.reconstruct(), (i, j)
