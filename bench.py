@@ -208,9 +208,11 @@ def middle_alg_bytes(L: int, S: int, TB: int = 32) -> int:
     """Bytes the middle kernel must move per solve (DESIGN 5.2): for every tile
     (I, J), J - I >= 2, split s' of its middle range and m, the fp32 shadow
     operands A32(s, s'-1, m) of its real rows s and C32(s', t, m - w) of its
-    real columns t are read once (4 B each) — the operand reuse a tile allows,
-    nothing re-read.  It writes no partial minima (its fired splits go to the
-    sub-product as lists of <= 32 uint16 per warp and 32 m, < 0.1% of this)."""
+    real columns t, and the quad minima of those rows / columns (one per 4,
+    the coarse bounds' operands), are read once (4 B each) — the operand reuse
+    a tile allows, nothing re-read.  It writes no partial minima (its fired
+    splits go to the sub-product as lists of <= 32 uint16 per warp and 32 m,
+    < 0.1% of this)."""
     n = L + 1
     nb = (n + TB - 1) // TB
     tot = 0
@@ -218,7 +220,7 @@ def middle_alg_bytes(L: int, S: int, TB: int = 32) -> int:
         cs = min(n, TB * (I + 1)) - TB * I
         for J in range(I + 2, nb):
             ct = min(n, TB * (J + 1)) - TB * J
-            tot += 4 * (cs + ct) * (J - I - 1) * TB
+            tot += 4 * (cs + ct + (cs + 3) // 4 + (ct + 3) // 4) * (J - I - 1) * TB
     return tot * (S + 1)
 
 
@@ -719,7 +721,8 @@ def run_ours(args):
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "peak_source": peak_kind,
                     "model": "middle_fp32_operand_bytes: the dominant kernel (pruned middle) against HBM on the "
-                             "bytes its tiling cannot avoid (fp32 shadow operands of every tile, split and m once); "
+                             "bytes its tiling cannot avoid (fp32 shadow operands of every tile, split and m once, with "
+                             "their quad minima); "
                              "NOT the wavefront model of SURVEY 8(d)",
                     "measured_in": f"{isolated['steps']} diagonal-schedule solves right after the timed region: the "
                                    "middle launches alone on the launch stream, CUDA events around each (library side)",
@@ -728,8 +731,9 @@ def run_ours(args):
                     "traffic_scope": "DRAM read+write bytes of all middle launches of one solve (ncu launch list, "
                                      "profiles/ncu_summary.json tiled_solve)",
                     "alg_bytes_per_step": mb_alg,
-                    "kernel": "k_tile_middle_wide (pruned middle: fp32 shadow boxes by bulk copy, coarse + per-cell "
-                              "exact lower-bound filter; fired splits handed to the sub-product)",
+                    "kernel": "k_tile_middle_wide (pruned middle: fp32 shadow rows + quad minima, two bulk copies "
+                              "per ring stage; coarse bounds from the quad minima, per-cell exact lower-bound "
+                              "filter; fired splits handed to the sub-product)",
                     "transitions_per_step": tm, "middle_ms_per_step": iso_ms,
                     "middle_launches_per_step": isolated["middle_launches"],
                     "middle_share_of_fill": iso_ms / isolated["fill_ms"],

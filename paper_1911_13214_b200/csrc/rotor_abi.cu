@@ -61,6 +61,7 @@ struct Layout {
     int64_t ops_cap = 0;
     size_t off_wx, off_wbx, off_wy, off_of, off_ob, off_P, off_w, off_mnull, off_stack, off_res;
     size_t off_chain, off_ops, off_C, off_D, off_A, off_C32, off_A32, off_tiled, off_ctr;
+    int64_t sarows = 0, scrows = 0;
     size_t total = 0;
     bool has_D = false;
     bool has_A = false;
@@ -113,8 +114,10 @@ Layout make_layout(int L, int S, const rotor_options &o) {
     y.off_D = y.has_D ? take((size_t)y.cells * y.pitch * 2) : 0;
     y.has_A = uses_tiled(o);
     y.off_A = y.has_A ? take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 8) : 0;
-    y.off_C32 = y.has_A ? take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 4) : 0;
-    y.off_A32 = y.has_A ? take((size_t)(y.cells + rotor::kPadRows) * y.pitch * 4) : 0;
+    y.scrows = rotor::shadow_rows_c(y.n);
+    y.sarows = rotor::shadow_rows_a(y.n);
+    y.off_C32 = y.has_A ? take((size_t)y.scrows * y.pitch * 4) : 0;
+    y.off_A32 = y.has_A ? take((size_t)y.sarows * y.pitch * 4) : 0;
     y.off_tiled = take(rotor::tiled_extra_bytes(L, S));
     y.total = off;
     return y;
@@ -142,7 +145,8 @@ rotor::Problem make_problem(const Layout &y, char *ws, const rotor_options &o) {
     p.A = y.has_A ? (double *)(ws + y.off_A) + rotor::kPad : nullptr;
     p.C32 = y.has_A ? (float *)(ws + y.off_C32) : nullptr;
     p.A32 = y.has_A ? (float *)(ws + y.off_A32) : nullptr;
-    p.srows = y.cells + rotor::kPadRows;
+    p.sarows = y.sarows;
+    p.scrows = y.scrows;
     p.counters = (y.has_A && o.counters) ? (unsigned long long *)(ws + y.off_ctr) : nullptr;
     p.flags = y.has_A ? (int *)(ws + y.off_tiled) : nullptr;
     p.mlist = y.has_A ? (uint16_t *)(ws + y.off_tiled + rotor::tiled_list_offset(y.L, y.S)) : nullptr;

@@ -71,8 +71,8 @@ __device__ __forceinline__ void leaf_cell(const Problem &p, int s, int m) {
     const double c = (m >= ma) ? p.w[s] : INFINITY;
     if (p.D) p.D[off] = (m >= ma) ? 0 : kNone;
     if (p.A) {
-        store_final_c(p, cell_index(p.n, s, s), m, p.wx[s - 1], c);
-        if (s < p.n) store_final_a(p, a_index(s, s), m, __dadd_rn(__dadd_rn(p.P[s], -p.P[s - 1]), c));
+        store_final_c(p, s, s, m, p.wx[s - 1], c);
+        if (s < p.n) store_final_a(p, s, s, m, __dadd_rn(__dadd_rn(p.P[s], -p.P[s - 1]), c));
     } else {
         p.C[off] = c;
     }

@@ -39,6 +39,7 @@ namespace rotor {
 namespace tiled {
 
 constexpr int TB = 32;      // tile edge in stages
+static_assert(TB == kTB, "the shadow layout's block edge is the tile edge");
 constexpr int KC = 8;       // splits per pipeline stage
 constexpr int TM = 16;      // m values per CTA (middle kernel)
 constexpr int STAGES = 3;   // TMA pipeline depth (2 stages in flight while one is consumed)
@@ -398,13 +399,16 @@ __device__ __forceinline__ void exact_flush(const Problem &p, const uint16_t *fl
     }
 }
 
+constexpr int SBOX = kSR * TMW;  // floats per split and operand: 32 cell rows + 8 quad-minima rows (5 KB)
 template <int KC_, int STAGES_>
 struct WideRing {
     static constexpr int KC = KC_, STAGES = STAGES_;
-    static constexpr int ST = 2 * KC * BOX;  // floats per stage: KC A boxes, then KC C boxes
+    static constexpr int NB = 2;  // bulk copies per stage: the KC splits' A rows, then their C rows
+    // floats per stage: [A: KC][kSR rows][TMW], [C: KC][kSR rows][TMW]
+    static constexpr int ST = 2 * KC * SBOX;
     // + the fired-split lists: NWARPS x fmax uint16 (wide_list_bytes)
     static constexpr size_t bytes =
-        (size_t)STAGES * ST * 4 + 2 * STAGES * 8 + (size_t)STAGES * 2 * KC * 8 + 2 * STAGES * 4 + 64;
+        (size_t)STAGES * ST * 4 + 2 * STAGES * 8 + (size_t)STAGES * NB * 8 + 2 * STAGES * 4 + 64;
 };
 // fired-split list length per warp: every split of the longest item
 // ((nb - 2) * TB), capped by FMAX_CAP and by the shared memory left next to
@@ -433,18 +437,18 @@ __device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t b
 enum { CTR_SPLITS = 0, CTR_COARSE_PASS = 1, CTR_QUADS = 2, CTR_EXACT = 3, CTR_WAIT = 4, CTR_INIT = 5, CTR_LOOP = 6,
        CTR_FLUSH = 7, CTR_N = 8 };
 
-template <int KCW, int STG, bool COUNT, int SS>
+template <int KCW, int STG, bool COUNT>
 __global__ void __launch_bounds__(THREADS, 1)
     k_tile_middle_wide(Problem p, int delta, int tile_lo, int n_tiles, int coarse, int fmax) {
     using R = WideRing<KCW, STG>;
-    constexpr int KC = R::KC, STAGES = R::STAGES, ST = R::ST;
+    constexpr int KC = R::KC, STAGES = R::STAGES, ST = R::ST, NB = R::NB;
     constexpr int NWARPS = CONSUMERS / 32;
     extern __shared__ __align__(1024) float fsm[];
     float *ring = fsm;  // [STAGES][A: KC][TB s][TMW] [C: KC][TB t][TMW]
     uint64_t *full = reinterpret_cast<uint64_t *>(ring + STAGES * ST);
     uint64_t *empty = full + STAGES;
-    const float **src = reinterpret_cast<const float **>(empty + STAGES);  // [STAGES][2 KC] next refill's boxes
-    int *claim = reinterpret_cast<int *>(src + STAGES * 2 * KC);  // step whose refill of the stage is unclaimed
+    const float **src = reinterpret_cast<const float **>(empty + STAGES);  // [STAGES][NB] next refill's boxes
+    int *claim = reinterpret_cast<int *>(src + STAGES * NB);  // step whose refill of the stage is unclaimed
     int *prep = claim + STAGES;                                   // step whose refill addresses are not yet computed
     int *wx_s = prep + STAGES;                                    // wx[0..n) when n <= WIDE_WX_MAX
     uint16_t *fl_s = reinterpret_cast<uint16_t *>(wx_s + (n_wx_smem(p.n) ? p.n : 0));  // [NWARPS][fmax]
@@ -471,17 +475,22 @@ __global__ void __launch_bounds__(THREADS, 1)
         m0 = (item % n_mc) * TMW;
         sp0 = i0 + TB + (gi % iters) * KC;
     };
+    // box 0 of a stage: the A32 rows (block I, columns sp0 - 1 .. sp0 + KC - 2),
+    // box 1: the C32 rows (block J, rows sp0 .. sp0 + KC - 1) — each split's 32
+    // cells + 8 quad minima, and the KC splits consecutive (srow_a / srow_c):
+    // one contiguous block each
+    auto box_src = [&](int b, int i0, int j0, int m0, int sp0) -> const float * {
+        return b == 0 ? p.A32 + shadow_index(p.sarows, sa_col(n, (i0 - 1) / TB, sp0 - 1), m0)
+                      : p.C32 + shadow_index(p.scrows, sc_row((j0 - 1) / TB, sp0), m0);
+    };
+    constexpr uint32_t box_bytes = KC * SBOX * 4;
     auto issue = [&](int gi) {
         const int st = gi % STAGES;
         int i0, j0, m0, sp0;
         coords(gi, i0, j0, m0, sp0);
         mbar_expect_tx(&full[st], (uint32_t)(ST * 4));
         float *dst = ring + st * ST;
-        for (int k = 0; k < KC; k++)  // A32(i0..i0+31, sp-1, m0..m0+31): rows a_index(i0.., sp-1) are consecutive
-            bulk_load(dst + k * BOX, p.A32 + shadow_index(p.srows, a_index(i0, sp0 + k - 1), m0), BOX * 4, &full[st]);
-        for (int k = 0; k < KC; k++)  // C32(sp, j0..j0+31, m0..): rows cell_index(sp, j0..) are consecutive
-            bulk_load(dst + (KC + k) * BOX, p.C32 + shadow_index(p.srows, cell_index(n, sp0 + k, j0), m0), BOX * 4,
-                      &full[st]);
+        for (int b = 0; b < NB; b++) bulk_load(dst + b * KC * SBOX, box_src(b, i0, j0, m0, sp0), box_bytes, &full[st]);
     };
     // Refills are split in two: the FIRST warp to finish reading a stage
     // computes the source addresses of its next refill (one box per lane,
@@ -489,19 +498,17 @@ __global__ void __launch_bounds__(THREADS, 1)
     // them.  The last arriver is the slowest warp; with the whole refill on it
     // (coordinates, 64-bit address arithmetic, copies) it had stayed the
     // slowest for good (the issuing warp at ~1.23x the others' loop cycles).
+    static_assert(NB <= 32, "one box per lane");
     auto prepare_warp = [&](int gi, int ln) {  // addresses of step gi's boxes
         int i0, j0, m0, sp0;
         coords(gi, i0, j0, m0, sp0);
-        if (ln < KC)
-            src[(gi % STAGES) * 2 * KC + ln] = p.A32 + shadow_index(p.srows, a_index(i0, sp0 + ln - 1), m0);
-        else if (ln < 2 * KC)
-            src[(gi % STAGES) * 2 * KC + ln] = p.C32 + shadow_index(p.srows, cell_index(n, sp0 + ln - KC, j0), m0);
+        if (ln < NB) src[(gi % STAGES) * NB + ln] = box_src(ln, i0, j0, m0, sp0);
     };
     auto issue_warp = [&](int gi, int ln) {  // lane 0 posts the expected bytes first
         const int st = gi % STAGES;
         if (ln == 0) mbar_expect_tx(&full[st], (uint32_t)(ST * 4));
         __syncwarp();
-        if (ln < 2 * KC) bulk_load(ring + st * ST + ln * BOX, src[st * 2 * KC + ln], BOX * 4, &full[st]);
+        if (ln < NB) bulk_load(ring + st * ST + ln * KC * SBOX, src[st * NB + ln], box_bytes, &full[st]);
     };
     if (tid == 0) {
         for (int s = 0; s < STAGES; s++) {
@@ -531,9 +538,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int kl = 0; kl < my_items; kl++) {
         const int item = (int)blockIdx.x + kl * (int)gridDim.x;
         const int I = tile_lo + item / n_mc, J = I + delta;
-        // the warp's 8 x 8 cells (s_0 + SS*i, t_0 + SS*j): SS = 1 a contiguous
-        // sub-tile, SS = 4 spread over the whole tile (balances the warps' work)
-        const int s_0 = I * TB + 1 + sg * (SS == 1 ? RW : 1), t_0 = J * TB + 1 + tg * (SS == 1 ? RW : 1);
+        // the warp's 8 x 8 cells (s_0 + i, t_0 + j): one contiguous sub-tile = two
+        // row groups x two column groups of the quad minima (a warp's cells spread
+        // over the tile balanced the warps' work but made the coarse test 2.5x
+        // weaker: 81.7 vs 67.4 ms of middle, removed)
+        const int s_0 = I * TB + 1 + sg * RW, t_0 = J * TB + 1 + tg * RW;
         const int m = (item % n_mc) * TMW + lane;
         const int mc = min(m, p.S);
         // bestf >= the exact partial minimum; -inf on cells whose partial is
@@ -543,8 +552,8 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int i = 0; i < RW; i++)
 #pragma unroll
             for (int j = 0; j < RW; j++) {
-                const int t = t_0 + SS * j;
-                bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + SS * i, t)) ? INFINITY : -INFINITY;
+                const int t = t_0 + j;
+                bestf[i][j] = (t <= n && m <= p.S && m >= m_null(p, s_0 + i, t)) ? INFINITY : -INFINITY;
             }
         float maxq[2][2];  // >= every bestf of the lane's 4 x 4 quadrants
 #pragma unroll
@@ -566,30 +575,34 @@ __global__ void __launch_bounds__(THREADS, 1)
             mbar_wait(&full[st], (uint32_t)((gi / STAGES) & 1));
             lap(c_wait);
             const float *a_f = ring + st * ST + (s_0 - I * TB - 1) * TMW + lane;
-            const float *b_f = ring + st * ST + KC * BOX + (t_0 - J * TB - 1) * TMW + lane;
+            const float *b_f = ring + st * ST + KC * SBOX + (t_0 - J * TB - 1) * TMW + lane;
+            // the warp's two row groups / two column groups among the quad minima
+            const float *qa_f = ring + st * ST + (kQuad + (s_0 - I * TB - 1) / 4) * TMW + lane;
+            const float *qb_f = ring + st * ST + KC * SBOX + (kQuad + (t_0 - J * TB - 1) / 4) * TMW + lane;
             unsigned needk = 0;
 #pragma unroll 1
             for (int k = 0; k < KC; k++) {
-                float a[RW], b[RW];
-#pragma unroll
-                for (int i = 0; i < RW; i++) a[i] = a_f[k * BOX + SS * i * TMW];
-#pragma unroll
-                for (int j = 0; j < RW; j++) b[j] = b_f[k * BOX + SS * j * TMW];
                 // coarse bounds first: per 4 x 4 quadrant (qa, qb) of the lane's
                 // tile, fadd_rd(min a over its rows, min b over its columns) is
                 // <= every lb of the quadrant (monotone rounding) and maxq >= every
                 // bestf of it; a quadrant is compared cell by cell only if that
-                // bound is below maxq on some lane of the warp
+                // bound is below maxq on some lane of the warp.  The minima come
+                // precomputed (QA / QC: 4 loads instead of 16 + 12 FMNMX).
                 float ma[2], mb[2];
 #pragma unroll
                 for (int h = 0; h < 2; h++) {
-                    ma[h] = fminf(fminf(a[4 * h], a[4 * h + 1]), fminf(a[4 * h + 2], a[4 * h + 3]));
-                    mb[h] = fminf(fminf(b[4 * h], b[4 * h + 1]), fminf(b[4 * h + 2], b[4 * h + 3]));
+                    ma[h] = qa_f[k * SBOX + h * TMW];
+                    mb[h] = qb_f[k * SBOX + h * TMW];
                 }
                 bool nk = false;
                 const float mall = fmaxf(fmaxf(maxq[0][0], maxq[0][1]), fmaxf(maxq[1][0], maxq[1][1]));
                 if (__any_sync(0xffffffffu, !coarse || __fadd_rd(fminf(ma[0], ma[1]), fminf(mb[0], mb[1])) < mall)) {
                     if (COUNT) c_coarse++;
+                    float a[RW], b[RW];
+#pragma unroll
+                    for (int i = 0; i < RW; i++) a[i] = a_f[k * SBOX + i * TMW];
+#pragma unroll
+                    for (int j = 0; j < RW; j++) b[j] = b_f[k * SBOX + j * TMW];
 #pragma unroll
                     for (int qa = 0; qa < 2; qa++)
 #pragma unroll
@@ -607,8 +620,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                                     }
                             }
                         }
-                }
-                if (__any_sync(0xffffffffu, nk)) {
+                  // (the whole warp is inside the coarse-pass branch: nk is uniform below)
+                  if (__any_sync(0xffffffffu, nk)) {
                     // The split may lower some cell: it is recorded for the exact fp64
                     // pass (deferred to the end of the item, so the warp does not stall
                     // on global memory here), and every bestf drops to an fp32 UPPER
@@ -639,6 +652,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                     maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
                         }
                     needk |= 1u << k;
+                  }
                 }
             }
             nf += __popc(needk);
@@ -666,11 +680,11 @@ __global__ void __launch_bounds__(THREADS, 1)
         // evaluates them exactly with its own splits; only an overflowing list
         // is evaluated here (and its exact partial written)
         uint16_t *gl = p.mlist + mlist_index(n_mc, I, item % n_mc, warp);
-        if (SS == 1 && nf <= MLIST_CAP) {
+        if (nf <= MLIST_CAP) {
             if (lane < nf) gl[1 + lane] = flist[lane];
             if (lane == 0) gl[0] = (uint16_t)nf;
         } else {
-            exact_flush(p, flist, nf, fmax, I * TB + 1 + TB, iters * KC, s_0, t_0, SS, m, mc, wxp);
+            exact_flush(p, flist, nf, fmax, I * TB + 1 + TB, iters * KC, s_0, t_0, 1, m, mc, wxp);
             if (lane == 0) gl[0] = MLIST_OVERFLOW;
         }
         __syncwarp();
@@ -690,6 +704,47 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 #include "rotor_tiled_dep.cuh"
+
+// Quad minima of the tiles I in [tile_lo, tile_lo + gridDim.z) of tile
+// diagonal delta, rebuilt from their fp32 shadows after a sharded fill unpacked
+// them (the leaves write them as they go): y < 256: the column groups of C32
+// row s = i0 + y / 8 (min of the 4 shadow rows at the same column: one row s,
+// one pre-shift); y >= 256: the row groups of A32 column c = j0 + (y - 256) / 8
+// (A(s, c) exists for s <= c, c < n).  Only existing cells enter a minimum; a
+// group with none gets +inf.  Thread = one shadow column m <= S.
+__global__ void k_tile_quads(Problem p, int delta, int tile_lo) {
+    const int n = p.n;
+    const int m = blockIdx.x * blockDim.x + threadIdx.x;
+    if (m > p.S) return;
+    const int I = tile_lo + (int)blockIdx.z, J = I + delta;
+    const int i0 = I * TB + 1, j0 = J * TB + 1;
+    const int y = blockIdx.y & 255, g = y & 7;
+    float v = INFINITY;
+    if (blockIdx.y < 256) {
+        const int s = i0 + (y >> 3), t1 = j0 + 4 * g;
+        if (s > n || j0 > n) return;  // no table row
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int t = t1 + k;
+            if (t >= s && t <= n) v = fminf(v, p.C32[shadow_index(p.scrows, srow_c(s, t), m)]);
+        }
+        p.C32[shadow_index(p.scrows, sc_row(J, s) + kQuad + g, m)] = v;
+    } else {
+        const int c = j0 + (y >> 3), s1 = i0 + 4 * g;
+        if (c >= n) return;  // no A column
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int s = s1 + k;
+            if (s <= c) v = fminf(v, p.A32[shadow_index(p.sarows, srow_a(n, s, c), m)]);
+        }
+        p.A32[shadow_index(p.sarows, sa_col(n, I, c) + kQuad + g, m)] = v;
+    }
+}
+
+inline void launch_quads(const Problem &p, int delta, int tile_lo, int ntiles, cudaStream_t st) {
+    dim3 grid((p.S + 1 + 127) / 128, 512, ntiles);
+    k_tile_quads<<<grid, 128, 0, st>>>(p, delta, tile_lo);
+}
 
 // ---------------------------------------------------------------------------
 // host side
@@ -723,32 +778,18 @@ template <int KCW, int STG>
 bool set_wide_attr() {
     const int b = 227 * 1024;
     const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
-    return cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, false, 1>, a, b) != cudaSuccess ||
-           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, true, 1>, a, b) != cudaSuccess ||
-           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, false, 4>, a, b) != cudaSuccess ||
-           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, true, 4>, a, b) != cudaSuccess;
+    return cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, false>, a, b) != cudaSuccess ||
+           cudaFuncSetAttribute(k_tile_middle_wide<KCW, STG, true>, a, b) != cudaSuccess;
 }
 
 template <int KCW, int STG>
 void launch_wide(const Problem &p, int delta, int tile_lo, int nt, int coarse, int grid, size_t wx_b, cudaStream_t st) {
     const int fmax = wide_fmax(p.n, WideRing<KCW, STG>::bytes);
     const size_t smem = WideRing<KCW, STG>::bytes + wx_b + (size_t)(CONSUMERS / 32) * fmax * 2;
-    static int ss = -1;  // ROTOR_WSPREAD=1: warps' cells spread over the tile (A/B)
-    if (ss < 0) {
-        const char *e = getenv("ROTOR_WSPREAD");
-        ss = (e && atoi(e)) ? 4 : 1;
-    }
-    if (ss == 4) {
-        if (p.counters)
-            k_tile_middle_wide<KCW, STG, true, 4><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
-        else
-            k_tile_middle_wide<KCW, STG, false, 4><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
-    } else {
-        if (p.counters)
-            k_tile_middle_wide<KCW, STG, true, 1><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
-        else
-            k_tile_middle_wide<KCW, STG, false, 1><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
-    }
+    if (p.counters)
+        k_tile_middle_wide<KCW, STG, true><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
+    else
+        k_tile_middle_wide<KCW, STG, false><<<grid, THREADS, smem, st>>>(p, delta, tile_lo, nt, coarse, fmax);
 }
 
 }  // namespace tiled
@@ -781,7 +822,7 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     static_assert(sizeof(CUtensorMap) <= sizeof(ctx->tmA), "tensor map storage");
     if (cudaFuncSetAttribute(k_tile_middle<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
-        set_wide_attr<4, 4>() || set_wide_attr<4, 6>() || set_wide_attr<2, 8>() || set_wide_attr<8, 3>())
+        set_wide_attr<4, 4>() || set_wide_attr<2, 8>())
         return -1;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -830,17 +871,13 @@ int tiled_delta_ep(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int 
             // carve-out to L1 (spill reloads, exact-pass operands)
             const size_t wx_b = n_wx_smem(p.n) ? (size_t)p.n * 4 : 0;
             const int gw = items_w < sms ? items_w : sms;
-            static int ring = -1;  // ROTOR_WRING=44|46|28|83 (KC x stages, A/B runs; default 4 x 4)
+            static int ring = -1;  // ROTOR_WRING=44|28 (KC x stages, A/B runs; default 4 x 4)
             if (ring < 0) {
                 const char *e = getenv("ROTOR_WRING");
                 ring = e ? atoi(e) : 44;
             }
-            if (ring == 46)
-                launch_wide<4, 6>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
-            else if (ring == 28)
+            if (ring == 28)
                 launch_wide<2, 8>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
-            else if (ring == 83)
-                launch_wide<8, 3>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
             else
                 launch_wide<WKC, WSTAGES>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
         } else {
@@ -984,8 +1021,8 @@ __global__ void k_tile_pack(Problem p, int delta, int tile_lo, double *buf, cons
     for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < W; m += gridDim.x * blockDim.x) {
         if (mode) {
             const double v = mode == 2 ? __ldcv(in + m) : in[m];  // .cv: the owner wrote it this diagonal
-            store_final_c(p, row, m, w, v);
-            if (has_a) store_final_a(p, a_index(s, t), m, __dadd_rn(u, v));
+            store_final_c(p, s, t, m, w, v);
+            if (has_a) store_final_a(p, s, t, m, __dadd_rn(u, v));
         } else {
             packed[m] = crow[m];
         }
@@ -996,14 +1033,17 @@ int tiled_pack(const Problem &p, int delta, int tile_lo, int tile_hi, double *bu
     if (tile_hi <= tile_lo) return 0;
     dim3 grid(4, tiled::TB * tiled::TB, tile_hi - tile_lo);
     k_tile_pack<<<grid, 256, 0, st>>>(p, delta, tile_lo, buf, nullptr, unpack ? 1 : 0);
-    return 1;
+    if (!unpack) return 1;
+    tiled::launch_quads(p, delta, tile_lo, tile_hi - tile_lo, st);
+    return 2;
 }
 
 int tiled_pull(const Problem &p, const double *src_C, int delta, int tile_lo, int tile_hi, cudaStream_t st) {
     if (tile_hi <= tile_lo) return 0;
     dim3 grid(4, tiled::TB * tiled::TB, tile_hi - tile_lo);
     k_tile_pack<<<grid, 256, 0, st>>>(p, delta, tile_lo, nullptr, src_C, 2);
-    return 1;
+    tiled::launch_quads(p, delta, tile_lo, tile_hi - tile_lo, st);
+    return 2;
 }
 
 }  // namespace rotor

@@ -234,111 +234,47 @@ __device__ __forceinline__ double finish(const Problem &p, int s, int t, int m, 
         const double v = __dadd_rn(p.w[s], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - p.wbx[s])]));
         c = dmin(c, v);
     }
-    store_final_c(p, cell_index(n, s, t), m, p.wx[s - 1], c);
+    store_final_c(p, s, t, m, p.wx[s - 1], c);
     const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), c);
-    if (t < n) store_final_a(p, a_index(s, t), m, a);
+    if (t < n) store_final_a(p, s, t, m, a);
     return a;
 }
 
-// One local row r of sub-tile (alpha, gamma) of tile I, at one m.  The lane
-// walks the row's SB cells left to right; right-range A operands stay in
-// registers.
-template <bool DIAG>
-__device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int alpha, int gamma, int I, int r,
-                                         int m) {
+// One local row r of the diagonal sub-tile (alpha, alpha) of diagonal tile I
+// (delta = 0, phase 0), at one m: cells (s, s+1..ea), splits s' in (s, t].  The
+// lane walks the row's cells left to right; right-range A operands stay in
+// registers.  (Off-diagonal sub-tiles: leaf_row_tab.)
+__device__ __forceinline__ void leaf_row_diag(const Problem &p, int alpha, int I, int r, int m) {
     const int n = p.n;
-    const int J = I + delta;
-    const int i0 = I * TB + 1, j0 = J * TB + 1;
-    const int s0 = i0 + SB * alpha, t0 = j0 + SB * gamma;
+    const int i0 = I * TB + 1;
+    const int s0 = i0 + SB * alpha, t0 = s0;
     const int s = s0 + r;
-    const int ea = s0 + SB - 1;  // last row of this row sub-block
-    if (s > n || t0 > n || m > p.S) return;  // sub-tiles past the last stage have no cells
+    if (s > n || m > p.S) return;  // sub-tiles past the last stage have no cells
     const int64_t pitch = p.pitch;
     double AR[SB + 1];  // AR[c] = A(s, t0 + c - 1)
-
-    if (DIAG) {  // diagonal sub-tile (delta = 0, e = 0): cells (s, s+1..ea), splits s' in (s, t]
-        if (s == n) return;  // the last stage's row has no cell right of its leaf
-        const double leaf = p.A[a_index(s, s) * pitch + m];  // the leaf (k_leaf, an earlier launch)
+    if (s == n) return;  // the last stage's row has no cell right of its leaf
+    const double leaf = p.A[a_index(s, s) * pitch + m];  // the leaf (k_leaf, an earlier launch)
 #pragma unroll
-        for (int c = 0; c < SB; c++)  // AR[r + 1] = leaf, with compile-time register indices
-            if (c == r) AR[c + 1] = leaf;
-#pragma unroll
-        for (int c = 0; c < SB; c++) {
-            if (c <= r) continue;
-            const int t = t0 + c;
-            if (t > n) break;
-            double c1 = INFINITY;
-            if (m >= m_null(p, s, t)) {  // every shifted index is >= 0 under this gate (DESIGN Q6)
-                double best = INFINITY;
-#pragma unroll
-                for (int cq = 0; cq < SB; cq++) {  // s' = t0 + cq + 1 in (s, t]
-                    if (cq < r || cq >= c) continue;
-                    const int sp = t0 + cq + 1;
-                    const double cv = __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])]);
-                    best = dmin(best, __dadd_rn(AR[cq + 1], cv));
-                }
-                c1 = best;
-            }
-            AR[c + 1] = finish(p, s, t, m, c1);
-        }
-        return;
-    }
-
-    // off-diagonal sub-tile: left s' in (s, ea], right s' in [t0, t]
-    const bool fAL = (delta == 0);  // left A: diagonal sub-tile of this tile (Delta = 0) or tile (I,I)
-    const bool fCR = (delta == 0);  // right C: diagonal sub-tile (gamma,gamma) (Delta = 0) or tile (J,J)
-    const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
-    AR[0] = __ldcg(&p.A[a_index(s, t0 - 1) * pitch + m]);
-    double AL[SB];  // AL[k] = A(s, s + k) for the left splits s' = s + k + 1 <= ea
-#pragma unroll
-    for (int k = 0; k < SB - 1; k++)
-        if (s + k + 1 <= ea) AL[k] = ld(&p.A[a_index(s, s + k) * pitch + m], fAL);
-    // pass 1 — independent across the row's cells (all loads in flight together):
-    // the partial, the left range (rows below), and the F_all operand.
-    double B[SB], F[SB];
-    bool gate[SB];
+    for (int c = 0; c < SB; c++)  // AR[r + 1] = leaf, with compile-time register indices
+        if (c == r) AR[c + 1] = leaf;
 #pragma unroll
     for (int c = 0; c < SB; c++) {
-        const int t = t0 + c;
-        gate[c] = t <= n && m >= m_null(p, s, t);  // every shifted index is >= 0 under it (DESIGN Q6)
-        double best = INFINITY;
-        if (gate[c]) {
-            best = partial ? __ldcg(&p.C[cell_index(n, s, t) * pitch + m]) : INFINITY;
-#pragma unroll
-            for (int k = 0; k < SB - 1; k++) {  // left: C of the rows below in this sub-tile (this Delta)
-                const int sp = s + k + 1;
-                if (sp > ea) break;
-                const double cv = __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])]);
-                best = dmin(best, __dadd_rn(AL[k], cv));
-            }
-        }
-        B[c] = best;
-        F[c] = (t <= n && !p.restricted && m >= m_all(p, s, t))  // row s+1 at m - wbx[s] >= 0, final
-                   ? __dadd_rn(p.w[s], __ldcg(&p.C[cell_index(n, s + 1, t) * pitch + (m - p.wbx[s])]))
-                   : INFINITY;
-    }
-    // pass 2 — the chain along the row: right range with the row's own A operands
-#pragma unroll
-    for (int c = 0; c < SB; c++) {
+        if (c <= r) continue;
         const int t = t0 + c;
         if (t > n) break;
         double c1 = INFINITY;
-        if (gate[c]) {
-            double best = B[c];
+        if (m >= m_null(p, s, t)) {  // every shifted index is >= 0 under this gate (DESIGN Q6)
+            double best = INFINITY;
 #pragma unroll
-            for (int cq = 0; cq < SB; cq++) {  // right: s' = t0 + cq <= t
-                if (cq > c) break;
-                const int sp = t0 + cq;
-                const double cv = ld(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])], fCR);
-                best = dmin(best, __dadd_rn(AR[cq], cv));
+            for (int cq = 0; cq < SB; cq++) {  // s' = t0 + cq + 1 in (s, t]
+                if (cq < r || cq >= c) continue;
+                const int sp = t0 + cq + 1;
+                const double cv = __ldcg(&p.C[cell_index(n, sp, t) * pitch + (m - p.wx[sp - 1])]);
+                best = dmin(best, __dadd_rn(AR[cq + 1], cv));
             }
             c1 = best;
         }
-        const double cc = dmin(c1, F[c]);
-        store_final_c(p, cell_index(n, s, t), m, p.wx[s - 1], cc);
-        const double a = __dadd_rn(__dadd_rn(p.P[t], -p.P[s - 1]), cc);
-        if (t < n) store_final_a(p, a_index(s, t), m, a);
-        AR[c + 1] = a;
+        AR[c + 1] = finish(p, s, t, m, c1);
     }
 }
 
@@ -347,20 +283,39 @@ __device__ __forceinline__ void leaf_row(const Problem &p, int delta, int e, int
 // m - shift, which may belong to lower m-chunks (other CTAs): after each row a
 // CTA publishes `flags[sub][chunk] = (phase_id << 4) | rows_done` (release) and
 // before each row waits (acquire) until every lower chunk of the same sub-tile
-// has done the rows below.  CTAs of lower chunks have lower blockIdx and never
-// wait on higher ones, so the chain always progresses (decoupled look-back).
+// has done the rows below (decoupled look-back).  A CTA's (sub-tile, chunk) is
+// not its blockIdx but a ticket drawn on arrival (leaf_ticket): every lower
+// ticket belongs to a CTA that is already resident, and lower chunks never wait
+// on higher ones, so the chain progresses whatever order the hardware
+// dispatches CTAs in.
 constexpr int LEAF_M = 128;
+
+// The launch's logical block index, in arrival order.  atomicInc wraps the
+// counter back to 0 on the launch's last ticket, so consecutive launches on
+// one counter (stream-ordered: each tile row / schedule has its own) need no
+// reset; the fill zeroes the counters once with the flags.
+__device__ __forceinline__ int leaf_ticket(unsigned *ticket) {
+    __shared__ int s_ticket;
+    if (threadIdx.x == 0) s_ticket = (int)atomicInc(ticket, gridDim.x - 1);
+    __syncthreads();
+    return s_ticket;
+}
 constexpr int NPAIR = SB * (SB + 1) / 2;  // right-range (column, split) pairs of a sub-tile row
 constexpr int LEAF_MIN_BLOCKS = 8;  // 32 warps/SM for the latency-bound leaf (<= 64 registers)
+#ifndef LEAF_RS_BLOCKS
+#define LEAF_RS_BLOCKS 5  // k_sub_leaf_row<true>: 36 KB of staged operands per CTA, <= 96 registers
+#endif
 
-template <bool DIAG>
-__global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf(Problem p, int delta, int e, int *flags, int phase_id,
-                                                        int tile_lo) {
+// (k_sub_leaf_diag: the diagonal sub-tiles of the diagonal tiles, delta = 0,
+// phase 0; k_sub_leaf_row: every other sub-tile.)
+__global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS)
+    k_sub_leaf_diag(Problem p, int delta, int e, int *flags, int phase_id, int tile_lo, unsigned *ticket) {
     const int n = p.n;
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int cnt = sub_count(delta, e);
-    const int q = blockIdx.x % n_chunks;
-    const int sub = blockIdx.x / n_chunks;  // tile I * cnt + sub-tile index
+    const int bid = leaf_ticket(ticket);
+    const int q = bid % n_chunks;
+    const int sub = bid / n_chunks;  // tile I * cnt + sub-tile index
     int alpha, gamma;
     sub_at(delta, e, sub % cnt, alpha, gamma);
     const int I = tile_lo + sub / cnt;
@@ -368,7 +323,6 @@ __global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf(Problem p,
     // flags of this sub-tile: indexed by the ABSOLUTE tile row I (tiles of
     // different launches may be in flight at once, each with its own epochs)
     int *my_flags = flags + ((int64_t)I * NSB + sub % cnt) * n_chunks;
-    (void)n;
     for (int r = SB - 1; r >= 0; r--) {
         if (r < SB - 1) {
             const int need = (phase_id << 4) | (SB - 1 - r);  // rows SB-1 .. r+1 done
@@ -380,11 +334,27 @@ __global__ void __launch_bounds__(LEAF_M, LEAF_MIN_BLOCKS) k_sub_leaf(Problem p,
             }
             __syncthreads();
         }
-        leaf_row<DIAG>(p, delta, e, alpha, gamma, I, r, m);
+        leaf_row_diag(p, alpha, I, r, m);
         __syncthreads();  // every thread of this chunk finished row r
         if (threadIdx.x == 0) {  // release (cumulative over the barrier): the chunk's row r is visible
             const int done = (phase_id << 4) | (SB - r);
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(my_flags + q), "r"(done) : "memory");
+        }
+    }
+    // The last column c = i0 + TB - 1 of a diagonal tile is the A operand of a
+    // middle's first split (s' = i0 + TB): its two bottom row groups lie in the
+    // last diagonal sub-tile (A(s, c), s < c, written above by this thread;
+    // A(c, c) by k_leaf), the others in off-diagonal sub-tiles (k_sub_leaf_row).
+    if (alpha == NSB - 1 && m <= p.S) {
+        const int s0 = I * TB + 1 + SB * alpha, c = s0 + SB - 1;
+        if (c < n) {
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                float v = INFINITY;
+#pragma unroll
+                for (int k = 0; k < 4; k++) v = fminf(v, p.A32[shadow_index(p.sarows, srow_a(n, s0 + 4 * h + k, c), m)]);
+                p.A32[shadow_index(p.sarows, sa_col(n, I, c) + kQuad + 2 * alpha + h, m)] = v;
+            }
         }
     }
 }
@@ -436,13 +406,15 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
 }
 
 // Off-diagonal leaf row r at one m (thread = m), scalars from the table; the
-// same arithmetic as leaf_row<false>.
+// same arithmetic as the wavefront's Eq. (2) for the in-sub-tile splits.
 // r: the row index as a compile-time constant (every loop trimmed and fully
 // unrolled: 8 row bodies, ~26 KB of SASS each; one runtime-row body, 3.6x less
 // code, measured slower in the tile-DAG schedule too: 143.2 vs 131.1 ms per solve)
+// qa: the running quad minima of the sub-tile's columns over the rows of the
+// current 4-row group (k_sub_leaf_row writes them after rows 4 and 0).
 template <int r, bool RS, class Wait>
 __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T, bool fresh, bool partial, int s0,
-                                             int t0, int m, bool live, const double *Rs, Wait wait) {
+                                             int t0, int m, bool live, const double *Rs, float (&qa)[SB], Wait wait) {
     const int n = p.n;
     const int64_t pitch = p.pitch;
     const int s = s0 + r;
@@ -484,13 +456,20 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     }
     if (RS) cp_async_wait<0>();  // this thread's right-range operands are in shared memory
     // the row's outputs, addressed incrementally: cells (s, t0+c) are consecutive
-    // C rows (their fp32 shadows consecutive shadow rows, pre-shifted by
-    // wx[s-1]); A(s, t) -> A(s, t+1) is t rows further on (a_index)
+    // C rows, and consecutive C32 shadow rows (pre-shifted by wx[s-1]) followed
+    // by the row's quad minima; A(s, t) -> A(s, t+1) is t rows further on
+    // (a_index), kSR shadow rows (srow_a)
     const int w = T.wself[r];
-    const int64_t c_row = cell_index(n, s, t0);
-    float *c32_hi = (m + w <= p.S) ? p.C32 + shadow_index(p.srows, c_row, m + w) : nullptr;
-    float *c32_lo = (m < w) ? p.C32 + shadow_index(p.srows, c_row, m) : nullptr;
+    const int J = (t0 - 1) / TB;
+    const int64_t c_row32 = sc_row(J, s) + (t0 - 1 - TB * J);
+    const int64_t q_row32 = sc_row(J, s) + kQuad + (t0 - 1 - TB * J) / 4;  // the row's two column groups
+    float *c32_hi = (m + w <= p.S) ? p.C32 + shadow_index(p.scrows, c_row32, m + w) : nullptr;
+    float *c32_lo = (m < w) ? p.C32 + shadow_index(p.scrows, c_row32, m) : nullptr;
+    float *q32_hi = (m + w <= p.S) ? p.C32 + shadow_index(p.scrows, q_row32, m + w) : nullptr;
+    float *q32_lo = (m < w) ? p.C32 + shadow_index(p.scrows, q_row32, m) : nullptr;
+    float qc[2] = {INFINITY, INFINITY};
     int64_t a_row = a_index(s, t0);
+    int64_t a_row32 = srow_a(n, s, t0);
 #pragma unroll
     for (int c = 0; c < SB; c++) {
         const int t = t0 + c;
@@ -509,15 +488,29 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
         }
         const double cc = dmin(c1, F[c]);
         Cm[crow + c * pitch] = cc;  // store_final_c, unrolled
-        if (c32_hi) c32_hi[c * kSW] = __double2float_rd(cc);
+        const float c32 = __double2float_rd(cc);
+        if (c32_hi) c32_hi[c * kSW] = c32;
         if (c32_lo) c32_lo[c * kSW] = INFINITY;
+        qc[c / 4] = fminf(qc[c / 4], c32);
         const double a = __dadd_rn(__dadd_rn(T.Pt[c], -T.Ps[r]), cc);
         if (t < n) {  // store_final_a
+            const float a32 = __double2float_rd(a);
             p.A[a_row * pitch + m] = a;
-            p.A32[shadow_index(p.srows, a_row, m)] = __double2float_rd(a);
+            p.A32[shadow_index(p.sarows, a_row32, m)] = a32;
+            qa[c] = fminf(qa[c], a32);
         }
         a_row += t;
+        a_row32 += kSR;
         AR[c + 1] = a;
+    }
+    // the row's two column-group minima (a group with no cell: +inf)
+    if (q32_hi) {
+        q32_hi[0] = qc[0];
+        q32_hi[kSW] = qc[1];
+    }
+    if (q32_lo) {
+        q32_lo[0] = INFINITY;
+        q32_lo[kSW] = INFINITY;
     }
 }
 
@@ -528,15 +521,16 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
 // the same for every row, are loaded once into shared memory (thread-private
 // columns, NPAIR x LEAF_M doubles) instead of once per row.
 template <bool RS>
-__global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_row(Problem p, int delta, int e, int *flags,
-                                                                        int phase_id, int tile_lo) {
+__global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS) k_sub_leaf_row(Problem p, int delta, int e, int *flags,
+                                                                        int phase_id, int tile_lo, unsigned *ticket) {
     __shared__ LeafTab T;
     extern __shared__ double Rsm[];  // [NPAIR][LEAF_M] when RS
     const int n = p.n;
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int cnt = sub_count(delta, e);
-    const int q = blockIdx.x % n_chunks;
-    const int sub = blockIdx.x / n_chunks;
+    const int bid = leaf_ticket(ticket);  // before any early exit: every CTA draws one
+    const int q = bid % n_chunks;
+    const int sub = bid / n_chunks;
     int alpha, gamma;
     sub_at(delta, e, sub % cnt, alpha, gamma);
     const int I = tile_lo + sub / cnt, J = I + delta;
@@ -545,7 +539,7 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
     const int m = q * LEAF_M + threadIdx.x;
     const bool fresh = (delta == 0);
     const bool partial = delta == 0 ? (e >= 2) : (delta >= 2 || alpha < NSB - 1 || gamma > 0);
-    int *my_flags = flags + ((int64_t)I * NSB + sub % cnt) * n_chunks;  // by absolute tile row (see k_sub_leaf)
+    int *my_flags = flags + ((int64_t)I * NSB + sub % cnt) * n_chunks;  // by absolute tile row (see k_sub_leaf_diag)
     leaf_tab_fill(p, s0, t0, q * LEAF_M, LEAF_M, T);
     const int q_lo = T.q_lo;
     if (RS) {
@@ -563,6 +557,10 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
             }
         cp_async_commit();
     }
+    float qa[SB];  // quad minima of the columns over the current 4-row group
+#pragma unroll
+    for (int c = 0; c < SB; c++) qa[c] = INFINITY;
+#pragma unroll
     for (int r = SB - 1; r >= 0; r--) {
         auto wait = [&]() {  // uniform over the CTA (every thread calls it once per row)
             if (r == SB - 1) return;
@@ -580,14 +578,22 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
             wait();
         } else {
             switch (r) {  // compile-time row index: the row's loops fully unrolled
-                case 0: leaf_row_tab<0, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
-                case 1: leaf_row_tab<1, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
-                case 2: leaf_row_tab<2, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
-                case 3: leaf_row_tab<3, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
-                case 4: leaf_row_tab<4, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
-                case 5: leaf_row_tab<5, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
-                case 6: leaf_row_tab<6, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
-                default: leaf_row_tab<7, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, wait); break;
+                case 0: leaf_row_tab<0, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+                case 1: leaf_row_tab<1, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+                case 2: leaf_row_tab<2, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+                case 3: leaf_row_tab<3, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+                case 4: leaf_row_tab<4, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+                case 5: leaf_row_tab<5, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+                case 6: leaf_row_tab<6, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+                default: leaf_row_tab<7, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+            }
+        }
+        if ((r & 3) == 0 && live) {  // rows r..r+3 done: the columns' quad minima (A(s, t) exists for t < n)
+            const int64_t q0 = sa_col(n, I, t0) + kQuad + (s0 - 1 - TB * I + r) / 4;
+#pragma unroll
+            for (int c = 0; c < SB; c++) {
+                if (t0 + c < n) p.A32[shadow_index(p.sarows, q0 + (int64_t)c * kSR, m)] = qa[c];
+                qa[c] = INFINITY;
             }
         }
         __syncthreads();
@@ -602,27 +608,27 @@ __global__ void __launch_bounds__(LEAF_M, RS ? 6 : LEAF_MIN_BLOCKS) k_sub_leaf_r
 // both the right-range operands and its own results in shared memory, 147 vs
 // 119 ms at the time; profiles/r01_tiled_v4.md, r01_tiled_v5.md.)
 
-// Flags of the leaf look-back: one int per (tile row I, sub-tile of a phase, m-chunk).
-inline size_t leaf_flag_bytes(int L, int S) {
+// Flags of the leaf look-back: one int per (tile row I, sub-tile of a phase,
+// m-chunk), then one ticket counter per tile row (indexed by the launch's
+// tile_lo: the DAG's row, the diagonal schedule's / a shard's first row).
+inline size_t leaf_flag_words(int L, int S) {
     const int nb = (L + 1 + TB - 1) / TB;
     const int chunks = (S + 1 + LEAF_M - 1) / LEAF_M;
-    return (size_t)nb * NSB * chunks * sizeof(int);
+    return (size_t)nb * NSB * chunks;
+}
+inline size_t leaf_flag_bytes(int L, int S) {
+    const int nb = (L + 1 + TB - 1) / TB;
+    return (leaf_flag_words(L, S) + nb) * sizeof(int);
 }
 
-// Off-diagonal leaf kernel: k_sub_leaf<false> (row: thread = m, scalars from
-// global), k_sub_leaf_row<false> (scalars staged in shared memory) or
-// k_sub_leaf_row<true> (also the right-range operands; the default, the fastest
-// measured); ROTOR_LEAF=row|tab|tabr selects one for A/B measurements.
-enum { LEAF_VARIANT_ROW = 0, LEAF_VARIANT_TAB = 1, LEAF_VARIANT_TABR = 2 };
-constexpr int LEAF_VARIANT_DEFAULT = LEAF_VARIANT_TABR;
-inline int leaf_variant() {
-    static const int v = [] {
+// Off-diagonal leaf kernel: k_sub_leaf_row<true> (the right-range operands
+// staged in shared memory; the default, the fastest measured) or
+// k_sub_leaf_row<false> (ROTOR_LEAF=tab, for A/B measurements).  (A third
+// variant with the scalars read from global memory was removed in round 2.)
+inline bool leaf_staged() {
+    static const bool v = [] {
         const char *e = getenv("ROTOR_LEAF");
-        if (!e) return (int)LEAF_VARIANT_DEFAULT;
-        if (!strcmp(e, "tab")) return (int)LEAF_VARIANT_TAB;
-        if (!strcmp(e, "tabr")) return (int)LEAF_VARIANT_TABR;
-
-        return (int)LEAF_VARIANT_ROW;
+        return !(e && !strcmp(e, "tab"));
     }();
     return v;
 }
@@ -674,15 +680,13 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
             launches++;
         }
         const int lb = ntiles * cnt * n_chunks;
+        unsigned *ticket = reinterpret_cast<unsigned *>(flags + leaf_flag_words(p.L, p.S)) + tile_lo;
         if (delta == 0 && e == 0)
-            k_sub_leaf<true><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
-        else if (leaf_variant() == LEAF_VARIANT_TAB)
-            k_sub_leaf_row<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
-        else if (leaf_variant() == LEAF_VARIANT_TABR)
-            k_sub_leaf_row<true><<<lb, LEAF_M, NPAIR * LEAF_M * 8, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
-
+            k_sub_leaf_diag<<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo, ticket);
+        else if (leaf_staged())
+            k_sub_leaf_row<true><<<lb, LEAF_M, NPAIR * LEAF_M * 8, st>>>(p, delta, e, flags, ++phase_id, tile_lo, ticket);
         else
-            k_sub_leaf<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo);
+            k_sub_leaf_row<false><<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo, ticket);
         launches++;
     }
     return launches;

@@ -196,9 +196,7 @@ print("ok")
 VARIANTS = {
     "exact": {"ROTOR_MIDDLE": "exact"},  # the unpruned fp64 k_tile_middle
     "nocoarse": {"ROTOR_COARSE": "0"},  # the pruned middle without its coarse bounds
-    "spread": {"ROTOR_WSPREAD": "1"},  # the pruned middle with each warp's cells spread over the tile
-    "ring46": {"ROTOR_WRING": "46"},  # the pruned middle with 6 ring stages
-    "leaf_row": {"ROTOR_LEAF": "row"},  # k_sub_leaf<false>: scalars from global memory
+    "ring28": {"ROTOR_WRING": "28"},  # the pruned middle with 8 ring stages of 2 splits
     "leaf_tab": {"ROTOR_LEAF": "tab"},  # k_sub_leaf_row<false>: right-range operands not staged
     "prod4": {"ROTOR_PROD": "1"},  # k_sub_product_async at 4 CTAs/SM
 }
