@@ -27,6 +27,7 @@
 #include <string.h>
 #include <limits.h>
 
+#include <chrono>
 #include <map>
 #include <vector>
 
@@ -966,6 +967,18 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st, int schedule, cudaEvent
         }
     } else {
         std::vector<int> phase(nb, 0);  // (middle launches are timed on their own streams; they overlap)
+        // ROTOR_TRACE=<file>: per tile task, the host enqueue time and the GPU
+        // time its middle starts / its dependent phase ends (timing events,
+        // relative to the fill's start) — a timeline of the DAG (diagnostic)
+        static const char *trace = getenv("ROTOR_TRACE");
+        std::vector<cudaEvent_t> tev;
+        std::vector<double> thost;
+        auto t_host0 = std::chrono::steady_clock::now();
+        cudaEvent_t tstart = nullptr;
+        if (trace) {
+            cudaEventCreate(&tstart);
+            cudaEventRecord(tstart, st);
+        }
         // row I on stream I mod ns: rows sharing a stream only add order between
         // tasks that are enqueued in dependency order anyway (diagonal-major)
         const int ns = (int)r->st.size();
@@ -979,12 +992,45 @@ int launch_fill_tiled(const Problem &p, cudaStream_t st, int schedule, cudaEvent
             for (int I = 0; I + delta < nb; I++) {
                 // (I+1, I+delta) is the latest record of ev[I+1]: row I+1 is enqueued after row I
                 if (delta >= 1) cudaStreamWaitEvent(row_st(I), r->ev[I + 1], 0);
-                launches += tiled_delta_ep(p, &ctx, delta, I, I + 1, row_st(I), phase[I]);
+                if (trace) {
+                    cudaEvent_t a, z;
+                    cudaEventCreate(&a);
+                    cudaEventCreate(&z);
+                    thost.push_back(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_host0).count());
+                    cudaEventRecord(a, row_st(I));
+                    launches += tiled_delta_ep(p, &ctx, delta, I, I + 1, row_st(I), phase[I]);
+                    cudaEventRecord(z, row_st(I));
+                    tev.push_back(a);
+                    tev.push_back(z);
+                } else {
+                    launches += tiled_delta_ep(p, &ctx, delta, I, I + 1, row_st(I), phase[I]);
+                }
                 cudaEventRecord(r->ev[I], row_st(I));
             }
             nvtxRangePop();
         }
         for (int I = 0; I < nb; I++) cudaStreamWaitEvent(st, r->ev[I], 0);  // (I < ns covers every stream)
+        if (trace) {
+            const double host_total =
+                std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t_host0).count();
+            cudaStreamSynchronize(st);
+            FILE *f = fopen(trace, "w");
+            if (f) {
+                fprintf(f, "I,J,host_us,start_us,end_us\n");
+                size_t k = 0;
+                for (int delta = 0; delta < nb; delta++)
+                    for (int I = 0; I + delta < nb; I++, k++) {
+                        float a = 0, z = 0;
+                        cudaEventElapsedTime(&a, tstart, tev[2 * k]);
+                        cudaEventElapsedTime(&z, tstart, tev[2 * k + 1]);
+                        fprintf(f, "%d,%d,%.1f,%.1f,%.1f\n", I, I + delta, thost[k], a * 1e3, z * 1e3);
+                    }
+                fprintf(f, "# host enqueue total %.1f us\n", host_total);
+                fclose(f);
+            }
+            for (auto e : tev) cudaEventDestroy(e);
+            cudaEventDestroy(tstart);
+        }
     }
     if (mid_n) *mid_n = ctx.mid_n;
     return launches;
