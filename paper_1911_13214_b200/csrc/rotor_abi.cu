@@ -939,6 +939,8 @@ struct ShardRank {
     char *ws = nullptr;
     cudaStream_t st = nullptr;
     cudaEvent_t ev_step = nullptr, ev_pack = nullptr, ev_copied = nullptr;
+    cudaStream_t xs = nullptr;         // exchange stream: this rank's receives of other ranks' tiles
+    cudaEvent_t ev_recv = nullptr;     // recorded on xs after a diagonal's foreign tiles landed
     rotor::Problem p{};
     rotor::TiledCtx ctx{};
     double *send[2] = {nullptr, nullptr}, *recv = nullptr;
@@ -986,6 +988,8 @@ int sharded_run(const rotor_chain *chain, int L, uint64_t M, int S, const rotor_
         CK(cudaEventCreateWithFlags(&q.ev_step, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&q.ev_pack, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&q.ev_copied, cudaEventDisableTiming));
+        CK(cudaStreamCreateWithFlags(&q.xs, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&q.ev_recv, cudaEventDisableTiming));
         if (stage_bytes) {
             q.send[0] = (double *)(q.ws + y.total);
             q.send[1] = (double *)(q.ws + y.total + cap * tb);
@@ -1000,7 +1004,15 @@ int sharded_run(const rotor_chain *chain, int L, uint64_t M, int S, const rotor_
         if (rotor::tiled_prepare(q.p, &q.ctx, q.st)) return fail(ROTOR_EDEVICE, "tiled setup failed on device %d", q.dev);
         CK(cudaEventRecord(q.ev_copied, q.st));
     }
-    std::vector<int> lo, hi;
+    // Pipelined per tile diagonal: a rank first computes the tiles whose two
+    // neighbours on the previous diagonal (tiles I and I+1) it computed itself
+    // — they overlap the previous diagonal's exchange, which runs on the
+    // rank's exchange stream xs — then waits for that exchange (ev_recv) and
+    // computes its edge tiles.  Every tile reads whole rows / columns of the
+    // diagonals before the previous one, which the wait of the previous
+    // iteration ordered in (Theorem 1 reads strictly shorter intervals,
+    // P:733-737; the same schedule as dist.solve_sharded).
+    std::vector<int> lo, hi, plo, phi;
     NvtxRange nv_fill("rotor.sharded.fill");
     for (int delta = 0; delta < nb; delta++) {
         char nm[48];
@@ -1010,11 +1022,27 @@ int sharded_run(const rotor_chain *chain, int L, uint64_t M, int S, const rotor_
         for (int r = 0; r < R; r++) {  // every rank: its share of the tiles of this diagonal
             ShardRank &q = rk[r];
             CK(cudaSetDevice(q.dev));
-            if (rotor::tiled_delta(q.p, &q.ctx, delta, lo[r], hi[r], q.st) < 0)
-                return fail(ROTOR_EDEVICE, "tiled step failed on device %d", q.dev);
-            CK(cudaGetLastError());
+            int a = lo[r], b = hi[r];  // the local span
+            if (delta > 0 && R > 1) {
+                a = std::max(lo[r], plo[r]);
+                b = std::min(hi[r], phi[r] - 1);
+                if (a >= b) a = b = lo[r];
+            }
+            auto step = [&](int l, int h) -> int {
+                if (h <= l) return ROTOR_OK;
+                if (rotor::tiled_delta(q.p, &q.ctx, delta, l, h, q.st) < 0)
+                    return fail(ROTOR_EDEVICE, "tiled step failed on device %d", q.dev);
+                CK(cudaGetLastError());
+                return ROTOR_OK;
+            };
+            int e = step(a, b);
+            if (e) return e;
+            if (delta > 0 && R > 1) CK(cudaStreamWaitEvent(q.st, q.ev_recv, 0));  // the previous diagonal's foreign tiles
+            if ((e = step(lo[r], a)) || (e = step(std::max(b, lo[r]), hi[r]))) return e;
             CK(cudaEventRecord(q.ev_step, q.st));
         }
+        plo = lo;
+        phi = hi;
         if (R == 1) continue;
         if (halo_mode == 0) {  // pack -> peer copy -> unpack
             const int b = delta & 1;
@@ -1023,7 +1051,7 @@ int sharded_run(const rotor_chain *chain, int L, uint64_t M, int S, const rotor_
                 if (hi[r] <= lo[r]) continue;
                 CK(cudaSetDevice(q.dev));
                 // send[b] was last read by the copies of delta - 2, which every
-                // receiver's stream ordered before its copies of delta - 1
+                // receiver's exchange stream ordered before its copies of delta - 1
                 for (int x = 0; x < R; x++)
                     if (x != r) CK(cudaStreamWaitEvent(q.st, rk[x].ev_copied, 0));
                 rotor::tiled_pack(q.p, delta, lo[r], hi[r], q.send[b], 0, q.st);
@@ -1035,12 +1063,13 @@ int sharded_run(const rotor_chain *chain, int L, uint64_t M, int S, const rotor_
                 CK(cudaSetDevice(q.dev));
                 for (int x = 0; x < R; x++) {
                     if (x == r || hi[x] <= lo[x]) continue;
-                    CK(cudaStreamWaitEvent(q.st, rk[x].ev_pack, 0));
-                    CK(cudaMemcpyPeerAsync(q.recv, q.dev, rk[x].send[b], rk[x].dev, (size_t)(hi[x] - lo[x]) * tb, q.st));
-                    rotor::tiled_pack(q.p, delta, lo[x], hi[x], q.recv, 1, q.st);
+                    CK(cudaStreamWaitEvent(q.xs, rk[x].ev_pack, 0));
+                    CK(cudaMemcpyPeerAsync(q.recv, q.dev, rk[x].send[b], rk[x].dev, (size_t)(hi[x] - lo[x]) * tb, q.xs));
+                    rotor::tiled_pack(q.p, delta, lo[x], hi[x], q.recv, 1, q.xs);
                     CK(cudaGetLastError());
                 }
-                CK(cudaEventRecord(q.ev_copied, q.st));
+                CK(cudaEventRecord(q.ev_copied, q.xs));
+                CK(cudaEventRecord(q.ev_recv, q.xs));
             }
         } else {  // fused P2P halo: each rank pulls the owners' tiles through peer memory
             for (int r = 0; r < R; r++) {
@@ -1048,12 +1077,17 @@ int sharded_run(const rotor_chain *chain, int L, uint64_t M, int S, const rotor_
                 CK(cudaSetDevice(q.dev));
                 for (int x = 0; x < R; x++) {
                     if (x == r || hi[x] <= lo[x]) continue;
-                    CK(cudaStreamWaitEvent(q.st, rk[x].ev_step, 0));
-                    rotor::tiled_pull(q.p, rk[x].p.C, delta, lo[x], hi[x], q.st);
+                    CK(cudaStreamWaitEvent(q.xs, rk[x].ev_step, 0));
+                    rotor::tiled_pull(q.p, rk[x].p.C, delta, lo[x], hi[x], q.xs);
                     CK(cudaGetLastError());
                 }
+                CK(cudaEventRecord(q.ev_recv, q.xs));
             }
         }
+    }
+    for (int r = 0; r < R && R > 1; r++) {  // the last diagonal's exchange
+        CK(cudaSetDevice(rk[r].dev));
+        CK(cudaStreamWaitEvent(rk[r].st, rk[r].ev_recv, 0));
     }
     // Algorithm 2 on the first rank's complete table
     ShardRank &q0 = rk[0];
@@ -1153,6 +1187,9 @@ int rotor_solve_sharded(const rotor_chain *chain, int32_t L, uint64_t mem_limit,
         if (q.ev_step) cudaEventDestroy(q.ev_step);
         if (q.ev_pack) cudaEventDestroy(q.ev_pack);
         if (q.ev_copied) cudaEventDestroy(q.ev_copied);
+        if (q.xs) cudaStreamSynchronize(q.xs);
+        if (q.ev_recv) cudaEventDestroy(q.ev_recv);
+        if (q.xs) cudaStreamDestroy(q.xs);
         if (q.st) cudaStreamDestroy(q.st);
     }
     cudaSetDevice(dev0);

@@ -495,10 +495,12 @@ __global__ void __launch_bounds__(THREADS, 1)
     };
     // Refills are split in two: the FIRST warp to finish reading a stage
     // computes the source addresses of its next refill (one box per lane,
-    // lane < 2 KC) into shared memory; the LAST one issues the copies from
+    // lane < NB) into shared memory; the LAST one issues the copies from
     // them.  The last arriver is the slowest warp; with the whole refill on it
     // (coordinates, 64-bit address arithmetic, copies) it had stayed the
     // slowest for good (the issuing warp at ~1.23x the others' loop cycles).
+    // Still true with two copies per stage: the last arriver computing its two
+    // addresses itself measured 48.6 vs 46.9 ms of middle per solve.
     static_assert(NB <= 32, "one box per lane");
     auto prepare_warp = [&](int gi, int ln) {  // addresses of step gi's boxes
         int i0, j0, m0, sp0;
@@ -950,6 +952,9 @@ DagRes *dag_res(int nb) {
 // middles — instead of every diagonal ending in a device-wide barrier.
 // Returns the number of kernels launched, or -1 on a launch/setup error.
 int launch_fill_tiled(const Problem &p, cudaStream_t st, int schedule, cudaEvent_t *mid_ev, int mid_cap, int *mid_n) {
+    // (A CUDA-graph replay of the whole DAG — one capture per problem, one
+    // cudaGraphLaunch per solve — measured no faster: 118.7 vs 118.9 ms per
+    // config-4 solve; the per-launch host and GPU gaps are not what bounds it.)
     TiledCtx ctx;
     if (tiled_prepare(p, &ctx, st)) return -1;
     ctx.mid_ev = mid_ev;

@@ -70,7 +70,34 @@ class CudaShardEngine:
         self.shard.pack(delta, lo, hi, buf, unpack=False, stream=self.stream)
 
     def unpack(self, delta, lo, hi, buf):
-        self.shard.pack(delta, lo, hi, buf, unpack=True, stream=self.stream)
+        """On the exchange stream (after the collective that filled `buf`)."""
+        self.shard.pack(delta, lo, hi, buf, unpack=True, stream=self.comm_stream())
+
+    # -- the exchange runs on its own stream, ordered against the compute
+    #    stream by events (solve_sharded's pipeline) --
+    def compute_stream(self):
+        t = self.torch
+        return self.stream if self.stream is not None else t.cuda.current_stream(self.dev)
+
+    def comm_stream(self):
+        if getattr(self, "_comm", None) is None:
+            self._comm = self.torch.cuda.Stream(device=self.dev)
+        return self._comm
+
+    def comm_after_compute(self):
+        """The exchange stream waits for everything enqueued on the compute stream so far (the pack)."""
+        ev = self.torch.cuda.Event()
+        ev.record(self.compute_stream())
+        self.comm_stream().wait_event(ev)
+
+    def compute_after_comm(self):
+        """The compute stream waits for the exchange stream (the unpacked tiles)."""
+        ev = self.torch.cuda.Event()
+        ev.record(self.comm_stream())
+        self.compute_stream().wait_event(ev)
+
+    def comm_context(self):
+        return self.torch.cuda.stream(self.comm_stream())
 
     def finish(self):
         t = self.torch
@@ -94,15 +121,20 @@ class CollectiveError(RuntimeError):
     """A per-diagonal exchange failed or timed out (a rank died, NCCL error, hang)."""
 
 
-def _all_gather_checked(recv, send, group, delta):
-    """all_gather_into_tensor as an async op, waited with a timeout: a failed or
-    hung peer surfaces as CollectiveError naming the tile diagonal instead of a
-    silent hang (NCCL's own async error handling aborts the communicator)."""
-    import datetime
-
+def _all_gather_start(recv, send, group):
     import torch.distributed as dist
 
-    work = dist.all_gather_into_tensor(recv, send, group=group, async_op=True)
+    return dist.all_gather_into_tensor(recv, send, group=group, async_op=True)
+
+
+def _all_gather_finish(work, delta):
+    """Wait for an all-gather started by _all_gather_start, with a timeout: a
+    failed or hung peer surfaces as CollectiveError naming the tile diagonal
+    instead of a silent hang (NCCL's own async error handling aborts the
+    communicator).  On NCCL the wait orders the CURRENT stream after the
+    collective (the host does not block); gloo blocks the host."""
+    import datetime
+
     try:
         ok = work.wait(timeout=datetime.timedelta(seconds=_collective_timeout()))
     except Exception as e:  # NCCL / gloo error reported by the backend
@@ -111,60 +143,152 @@ def _all_gather_checked(recv, send, group, delta):
         raise CollectiveError(f"all-gather of tile diagonal {delta} timed out after {_collective_timeout()} s")
 
 
+def _all_gather_checked(recv, send, group, delta):
+    _all_gather_finish(_all_gather_start(recv, send, group), delta)
+
+
+def local_span(ranges, prev_ranges, rank):
+    """The tiles [a, b) of this rank's range on a tile diagonal whose two
+    neighbours on the previous diagonal (tile I and I+1: (I, J-1) and (I+1, J))
+    it computed itself, so they need nothing from that diagonal's exchange."""
+    lo, hi = ranges[rank]
+    if prev_ranges is None:
+        return lo, hi
+    plo, phi = prev_ranges[rank]
+    a, b = max(lo, plo), min(hi, phi - 1)
+    return (a, b) if a < b else (lo, lo)
+
+
+def _nullcontext():
+    import contextlib
+
+    return contextlib.nullcontext()
+
+
 def solve_sharded(engine, group=None):
     """one table sharded over the ranks of `group`.
 
     Per tile diagonal delta (every tile of which depends only on smaller
-    diagonals): each rank computes a contiguous range of the tiles,
+    diagonals) each rank computes a contiguous range of the tiles,
     packs them, the ranks all-gather the packed tiles (NCCL over NVLink on
-    GPUs, gloo in the CPU tests), and every rank unpacks the others' tiles, so
+    GPUs, gloo in the CPU tests) and every rank unpacks the others' tiles, so
     each rank ends with the full table and runs Algorithm 2 itself.
-    `engine` provides nb, tile_bytes, step, pack, unpack, buffer, finish.
+
+    The exchange of diagonal delta overlaps the compute of delta + 1: tile I of
+    delta + 1 reads tiles I and I+1 of delta (its left / lower neighbours) and
+    whole rows / columns of diagonals <= delta - 1, so the tiles whose two
+    neighbours this rank computed itself (local_span: all but the range's
+    edges) start at once, and only the edge tiles wait for delta's unpacked
+    tiles.  The all-gather and the unpacks run on the engine's exchange
+    stream, ordered against the compute stream by events; the send / receive
+    buffers alternate between two sets (delta's are free again once delta + 1
+    waited for its unpack).
+
+    `engine` provides nb, tile_bytes, step, pack, unpack, buffer, finish and
+    (optional: absent in the CPU tests) comm_after_compute, compute_after_comm,
+    comm_context.
     """
     import torch.distributed as dist
 
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     tb = engine.tile_bytes
+    after_compute = getattr(engine, "comm_after_compute", lambda: None)
+    after_comm = getattr(engine, "compute_after_comm", lambda: None)
+    comm_ctx = getattr(engine, "comm_context", _nullcontext)
+    pending = None  # (delta, ranges, cap, recv, work) of the exchange in flight
+
+    def complete(p):
+        d, rngs, cap, recv, work = p
+        with comm_ctx():
+            _all_gather_finish(work, d)
+            for r, (l, h) in enumerate(rngs):
+                if r != rank and h > l:
+                    engine.unpack(d, l, h, recv[r * cap * tb: (r * cap + (h - l)) * tb])
+        after_comm()
+
     for delta in range(engine.nb):
         ranges = tile_ranges(engine.nb - delta, world)
         lo, hi = ranges[rank]
-        engine.step(delta, lo, hi)
         if world == 1:
+            engine.step(delta, lo, hi)
             continue
+        a, b = local_span(ranges, pending[1] if pending else None, rank)
+        if b > a:
+            engine.step(delta, a, b)  # overlaps the exchange of delta - 1
+        if pending:
+            complete(pending)
+        if a > lo:
+            engine.step(delta, lo, a)
+        if hi > b and b >= a:
+            engine.step(delta, max(b, lo), hi)
         cap = max(h - l for l, h in ranges)
-        send = engine.buffer("send", cap)
+        send = engine.buffer(f"send{delta & 1}", cap)
         engine.pack(delta, lo, hi, send)
-        recv = engine.buffer("recv", cap * world)
-        _all_gather_checked(recv, send, group, delta)
-        for r, (l, h) in enumerate(ranges):
-            if r != rank and h > l:
-                engine.unpack(delta, l, h, recv[r * cap * tb: (r * cap + (h - l)) * tb])
+        recv = engine.buffer(f"recv{delta & 1}", cap * world)
+        after_compute()
+        with comm_ctx():
+            work = _all_gather_start(recv, send, group)
+        pending = (delta, ranges, cap, recv, work)
+    if pending:
+        complete(pending)
     return engine.finish()
 
 
 def solve_sharded_virtual(engines):
-    """The same schedule with len(engines) ranks emulated in one process (the
-    all-gather becomes direct unpacks of the other engines' send buffers)."""
+    """The same pipelined schedule with len(engines) ranks emulated in one
+    process: the all-gather becomes each engine unpacking the other engines'
+    send buffers on its exchange stream, after their packs (events), while the
+    local tiles of the next diagonal run on its compute stream."""
     world = len(engines)
     nb = engines[0].nb
     tb = engines[0].tile_bytes
+    pending = None  # (delta, ranges, sends)
+
+    def complete(p):
+        d, rngs, sends = p
+        for r, e in enumerate(engines):
+            if hasattr(e, "comm_stream"):
+                for q, f in enumerate(engines):  # r's exchange stream after every rank's pack
+                    if q != r:
+                        e.comm_stream().wait_event(f._packed)
+            with (e.comm_context() if hasattr(e, "comm_context") else _nullcontext()):
+                for q, (l, h) in enumerate(rngs):
+                    if q != r and h > l:
+                        e.unpack(d, l, h, sends[q][: (h - l) * tb])
+            if hasattr(e, "compute_after_comm"):
+                e.compute_after_comm()
+
     for delta in range(nb):
         ranges = tile_ranges(nb - delta, world)
-        for r, e in enumerate(engines):
-            e.step(delta, *ranges[r])
         if world == 1:
+            engines[0].step(delta, *ranges[0])
             continue
+        spans = [local_span(ranges, pending[1] if pending else None, r) for r in range(world)]
+        for r, e in enumerate(engines):
+            a, b = spans[r]
+            if b > a:
+                e.step(delta, a, b)
+        if pending:
+            complete(pending)
         cap = max(h - l for l, h in ranges)
         sends = []
         for r, e in enumerate(engines):
-            s = e.buffer("send", cap)
-            e.pack(delta, *ranges[r], s)
-            sends.append(s)
-        for r, e in enumerate(engines):
-            for q, (l, h) in enumerate(ranges):
-                if q != r and h > l:
-                    e.unpack(delta, l, h, sends[q][: (h - l) * tb])
+            lo, hi = ranges[r]
+            a, b = spans[r]
+            if a > lo:
+                e.step(delta, lo, a)
+            if hi > b and b >= a:
+                e.step(delta, max(b, lo), hi)
+            snd = e.buffer(f"send{delta & 1}", cap)
+            e.pack(delta, lo, hi, snd)
+            if hasattr(e, "compute_stream"):
+                e._packed = e.torch.cuda.Event()
+                e._packed.record(e.compute_stream())
+            sends.append(snd)
+        pending = (delta, ranges, sends)
+    if pending:
+        complete(pending)
     return [e.finish() for e in engines]
 
 

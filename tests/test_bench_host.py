@@ -36,7 +36,8 @@ def test_middle_transitions_bruteforce():
 
 
 def test_middle_alg_bytes_bruteforce():
-    """fp32 operand reads (one per real row / column, split and m), enumerated tile by tile."""
+    """fp32 operand reads (one per real row / column, split and m) and their quad
+    minima (one per group of 4 real rows / columns), enumerated tile by tile."""
     TB = 32
     for L, S in ((70, 3), (130, 2)):
         n = L + 1
@@ -47,7 +48,8 @@ def test_middle_alg_bytes_bruteforce():
             for J in range(I + 2, nb):
                 cols = [t for t in range(TB * J + 1, TB * J + TB + 1) if t <= n]
                 splits = range(TB * (I + 1) + 1, TB * J + 1)
-                brute += sum(4 * len(rows) + 4 * len(cols) for _ in splits)
+                groups = len({(s - 1) // 4 for s in rows}) + len({(t - 1) // 4 for t in cols})
+                brute += sum(4 * len(rows) + 4 * len(cols) + 4 * groups for _ in splits)
         assert bench.middle_alg_bytes(L, S, TB) == brute * (S + 1)
 
 

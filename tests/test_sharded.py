@@ -150,6 +150,33 @@ def test_tile_ranges():
             assert max(sizes) - min(sizes) <= 1
 
 
+def test_local_span():
+    """The tiles a rank computes before the previous diagonal's exchange lands:
+    both neighbours (tile I and I+1 of the previous diagonal) are its own, and
+    the rest of its range is contiguous around them."""
+    from paper_1911_13214_b200.dist import local_span, tile_ranges
+
+    for nb in (1, 2, 5, 17, 32, 40):
+        for w in range(1, 9):
+            prev = None
+            for d in range(nb):
+                rs = tile_ranges(nb - d, w)
+                for r in range(w):
+                    lo, hi = rs[r]
+                    a, b = local_span(rs, prev, r)
+                    assert lo <= a <= b <= hi
+                    if prev is None:
+                        assert (a, b) == (lo, hi)
+                        continue
+                    plo, phi = prev[r]
+                    for I in range(a, b):
+                        assert plo <= I and I + 1 < phi
+                    for I in range(lo, hi):  # every tile with both neighbours local is in the span
+                        if plo <= I and I + 1 < phi:
+                            assert a <= I < b
+                prev = rs
+
+
 @pytest.mark.gpu
 @pytest.mark.parametrize("world", [2, 3])
 def test_sharded_virtual_ranks_gpu(world, oracle_mod):
