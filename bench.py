@@ -408,6 +408,13 @@ def run_batched(args):
                    "sample": f"oracle solves of every {stride}th limit of each of the 8 chains "
                              f"({len(chains) * len(js)} tables, {trc:.3e} transitions, {dtc:.1f} s, "
                              f"OpenMP over the cells of a diagonal on {HOST_CORES} cores)"}
+        kb_traffic = None
+        if world == 1:
+            try:
+                with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+                    kb_traffic = json.load(f)["k_batch"]["dram_bytes_per_launch"]
+            except Exception:
+                kb_traffic = None
         line = {"metric": "DP cell-transitions/sec, batched 256-limit x 8-chain sweep (config 5)",
                 "value": tot * args.steps / sec, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps,
@@ -417,7 +424,10 @@ def run_batched(args):
                                                  "note": "host-buffer API: H2D chains/limits and D2H costs+ops inside the timed region"},
                 "clocks": clk,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
+                             "frac": achieved / peak, "traffic": kb_traffic, "peak_source": peak_kind,
+                             "traffic_over_alg": (kb_traffic / tot_bytes) if kb_traffic else None,
+                             "traffic_scope": "DRAM read+write bytes of the one k_batch launch of a step, one ncu "
+                                              "--set full capture (profiles/ncu_summary.json k_batch); null for N > 1",
                              "kernel": "k_batch (fused: discretise, limits, wavefront fill, Algorithm 2 per table)",
                              "alg_bytes_per_step": tot_bytes},
                 "cpu_baseline": cpu, "gpu_launches": args.steps * world}
