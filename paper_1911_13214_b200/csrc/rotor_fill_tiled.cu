@@ -419,7 +419,7 @@ inline int wide_fmax(int n, size_t ring_bytes) {
     const int room = (int)((227 * 1024 - ring_bytes - wx_b) / ((CONSUMERS / 32) * 2)) & ~7;
     return max(8, min(min(FMAX_CAP, room), max(1, ((n + TB - 1) / TB - 2) * TB)));
 }
-constexpr int WKC = 4, WSTAGES = 4;  // ring of the wide middle (see tiled_delta)
+constexpr int WKC = 8, WSTAGES = 2;  // ring of the wide middle (see tiled_delta)
 constexpr int WIDE_WX_MAX = 4096;  // wx staged in shared memory up to this n (wide_fmax agrees)
 __host__ __device__ inline bool n_wx_smem(int n) { return n <= WIDE_WX_MAX; }
 static_assert((TB / RW) * (TB / RW) * TMW == THREADS, "one lane per (m, 8x8 tile)");
@@ -825,7 +825,7 @@ int tiled_prepare(const Problem &p, TiledCtx *ctx, cudaStream_t st) {
     static_assert(sizeof(CUtensorMap) <= sizeof(ctx->tmA), "tensor map storage");
     if (cudaFuncSetAttribute(k_tile_middle<KC, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)(SMEM_BYTES + (size_t)WX_SMEM_MAX * 4)) != cudaSuccess ||
-        set_wide_attr<4, 4>() || set_wide_attr<2, 8>())
+        set_wide_attr<8, 2>() || set_wide_attr<4, 4>() || set_wide_attr<2, 8>() || set_wide_attr<4, 2>())
         return -1;
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
@@ -874,13 +874,20 @@ int tiled_delta_ep(const Problem &p, TiledCtx *ctx, int delta, int tile_lo, int 
             // carve-out to L1 (spill reloads, exact-pass operands)
             const size_t wx_b = n_wx_smem(p.n) ? (size_t)p.n * 4 : 0;
             const int gw = items_w < sms ? items_w : sms;
-            static int ring = -1;  // ROTOR_WRING=44|28 (KC x stages, A/B runs; default 4 x 4)
+            // ROTOR_WRING=44|28|42 (KC x stages, A/B runs; default 8 x 2: half the
+            // release / refill rounds per split of 4 x 4 — 41.9 vs 46.8 ms of
+            // middle per config-4 solve; 4 x 3 45.8)
+            static int ring = -1;
             if (ring < 0) {
                 const char *e = getenv("ROTOR_WRING");
-                ring = e ? atoi(e) : 44;
+                ring = e ? atoi(e) : 82;
             }
             if (ring == 28)
                 launch_wide<2, 8>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
+            else if (ring == 44)
+                launch_wide<4, 4>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
+            else if (ring == 42)
+                launch_wide<4, 2>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
             else
                 launch_wide<WKC, WSTAGES>(p, delta, tile_lo, nt, coarse, gw, wx_b, st);
         } else {

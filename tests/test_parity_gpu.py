@@ -197,6 +197,7 @@ VARIANTS = {
     "exact": {"ROTOR_MIDDLE": "exact"},  # the unpruned fp64 k_tile_middle
     "nocoarse": {"ROTOR_COARSE": "0"},  # the pruned middle without its coarse bounds
     "ring28": {"ROTOR_WRING": "28"},  # the pruned middle with 8 ring stages of 2 splits
+    "ring44": {"ROTOR_WRING": "44"},  # 4 ring stages of 4 splits (the default before the 8 x 2 ring)
     "leaf_tab": {"ROTOR_LEAF": "tab"},  # k_sub_leaf_row<false>: right-range operands not staged
     "prod4": {"ROTOR_PROD": "1"},  # k_sub_product_async at 4 CTAs/SM
 }
