@@ -569,6 +569,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
                     for (int j = 4 * qb; j < 4 * qb + 4; j++) maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
             }
+        // >= every bestf of the lane's tile (kept with maxq: changes only when a split fires)
+        float mall = fmaxf(fmaxf(maxq[0][0], maxq[0][1]), fmaxf(maxq[1][0], maxq[1][1]));
         int nf = 0;  // fired splits of this item (warp-uniform; > fmax: the list overflowed)
         lap(c_init);
         for (int it = 0; it < iters; it++) {
@@ -598,7 +600,6 @@ __global__ void __launch_bounds__(THREADS, 1)
                     mb[h] = qb_f[k * SBOX + h * TMW];
                 }
                 bool nk = false;
-                const float mall = fmaxf(fmaxf(maxq[0][0], maxq[0][1]), fmaxf(maxq[1][0], maxq[1][1]));
                 if (__any_sync(0xffffffffu, !coarse || __fadd_rd(fminf(ma[0], ma[1]), fminf(mb[0], mb[1])) < mall)) {
                     if (COUNT) c_coarse++;
                     float a[RW], b[RW];
@@ -654,6 +655,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                                 for (int j = 4 * qb; j < 4 * qb + 4; j++)
                                     maxq[qa][qb] = fmaxf(maxq[qa][qb], bestf[i][j]);
                         }
+                    mall = fmaxf(fmaxf(maxq[0][0], maxq[0][1]), fmaxf(maxq[1][0], maxq[1][1]));
                     needk |= 1u << k;
                   }
                 }
