@@ -585,7 +585,7 @@ __global__ void __launch_bounds__(THREADS, 1)
             const float *qa_f = ring + st * ST + (kQuad + (s_0 - I * TB - 1) / 4) * TMW + lane;
             const float *qb_f = ring + st * ST + KC * SBOX + (kQuad + (t_0 - J * TB - 1) / 4) * TMW + lane;
             unsigned needk = 0;
-#pragma unroll 1
+#pragma unroll 2
             for (int k = 0; k < KC; k++) {
                 // coarse bounds first: per 4 x 4 quadrant (qa, qb) of the lane's
                 // tile, fadd_rd(min a over its rows, min b over its columns) is
