@@ -7,4 +7,4 @@ TAG=${1:-ev}; OUT=gpurun_out/$TAG; mkdir -p "$OUT"
 bash scripts/gpu_round.sh "$TAG" tests,smoke,bench
 bash scripts/gpu_profile_r02b.sh "$TAG/prof"
 ROTOR_TRACE="$OUT/dag_trace.csv" timeout 300 python scripts/time_solve.py dag 2 > "$OUT/trace.log" 2>&1; echo "trace rc=$?"
-bash scripts/sanitize.sh "$TAG/san" 2>&1 | tail -4
+if [ -n "${SAN:-}" ]; then bash scripts/sanitize.sh "$TAG/san" 2>&1 | tail -4; fi  # compute-sanitizer is closed on this pool
