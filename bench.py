@@ -719,6 +719,17 @@ def run_ours(args):
         mb_alg = middle_alg_bytes(L, S)
         peak = float(peaks["hbm_gbs"])
         alu_peak = 148 * 64.0 * clk_mhz * 1e6 / 1e9  # Gcandidates/s, one FSETP per candidate
+        dep_roof = None
+        if work and isolated:
+            dep_ms = isolated["fill_ms"] - isolated["middle_ms"]
+            dep_work = work["dependent_exact"] + work["middle_exact_candidates"]
+            dep_peak = 148 * 21.33 * clk_mhz * 1e6 / 1e9
+            dep_ach = dep_work / (dep_ms / 1e3) / 1e9
+            dep_roof = {"bound": "alu", "achieved": dep_ach, "peak": dep_peak, "frac": dep_ach / dep_peak,
+                        "unit": "Gtransitions/s", "ms_per_step": dep_ms, "exact_candidates_per_step": dep_work,
+                        "kernels": "k_sub_product_async + k_sub_leaf_row (+ k_sub_leaf_diag)",
+                        "note": "latency-bound: the leaves chain 8 rows per sub-tile through cross-CTA look-back "
+                                "flags, the sub-products stream fp64 operands from HBM at 12 warps per SM"}
         # the whole fill against the exact fp64 evaluation model (DADD 64 lanes/clk +
         # DSETP 32 lanes/clk per SM on the fp64 pipe -> 21.33 transitions/clk/SM)
         fill_peak = 148 * (64.0 / 3.0) * clk_mhz * 1e6 / 1e9
@@ -755,11 +766,20 @@ def run_ours(args):
                                   "unit": "Gtransitions/s",
                                   "peak_model": "148 SMs x sm_max_mhz x 64 candidates/clk/SM (one FSETP per "
                                                 "candidate on the ALU pipe; the coarse bounds skip most of them)"},
-                    "fill": {"achieved": fill_ach, "peak": fill_peak, "frac": fill_ach / fill_peak,
+                    # the whole fill: NOMINAL transitions per second (what `value` counts) beside
+                    # the exact-evaluation peak — a pruned fill evaluates only a fraction of them,
+                    # so this ratio is a speed-up over evaluating every candidate, not a fraction
+                    # of a peak (`dependent` below is the honest one for the exact phase)
+                    "fill": {"achieved_nominal": fill_ach, "exact_eval_peak": fill_peak,
+                             "nominal_over_exact_peak": fill_ach / fill_peak,
                              "unit": "Gtransitions/s", "ms_per_step": fill_avg_ms, "launches_per_step": fill_launches,
                              "peak_model": "148 SMs x sm_max_mhz x 21.33 transitions/clk/SM (exact fp64 evaluation: "
                                            "DADD 64 + DSETP 32 lanes/clk/SM, scripts/microbench_minplus.cu)",
                              "traffic": ncu_step_traffic("tiled_solve")},
+                    # the dependent phase (sub-products + leaves, every candidate exact in fp64,
+                    # the middle's fired splits included) against the same fp64 peak; its time =
+                    # fill - middle in the diagonal-schedule solves of `isolated`
+                    "dependent": dep_roof,
                     # SURVEY 8(d)'s own model: a diagonal-synchronous wavefront must move B_alg
                     # bytes; the blocked fill reuses data across diagonals, so the solve beats
                     # that floor -- reported as a speed-up, not as a fraction of a peak
