@@ -235,6 +235,27 @@ def ncu_kernel_step_traffic(key: str, kernel: str):
         return None
 
 
+def ncu_kernel_shares(key: str):
+    """Each kernel's share of one solve's serialised ncu time and DRAM bytes (committed launch list):
+    which kernel dominates.  The roofline above is the middle's — the heaviest per launch and in DRAM
+    traffic, the kernel the round-1 verdict named; the leaf takes more total time in the diagonal
+    schedule and is latency-bound (`dependent` reports that phase against the fp64 pipe)."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            ent = json.load(f)[key]
+        tot_ms = sum(v["ms"] for v in ent["per_kernel"].values())
+        tot_b = sum(v["dram_bytes"] for v in ent["per_kernel"].values())
+        out = {}
+        for k, v in ent["per_kernel"].items():
+            name = k.replace("void ", "").replace("tiled::", "").split("<")[0]
+            out[name] = {"time_share": round(v["ms"] / tot_ms, 4), "dram_share": round(v["dram_bytes"] / tot_b, 4)}
+        out["source"] = ent.get("source")
+        return out
+    except Exception:
+        return None
+
+
 def ncu_step_traffic(key: str):
     """DRAM read+write bytes of all launches of one solve, from the committed ncu launch list summary."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -752,6 +773,7 @@ def run_ours(args):
                     "traffic_scope": "DRAM read+write bytes of all middle launches of one solve (ncu launch list, "
                                      "profiles/ncu_summary.json tiled_solve)",
                     "alg_bytes_per_step": mb_alg,
+                    "kernel_shares": ncu_kernel_shares("tiled_solve"),
                     "kernel": "k_tile_middle_wide (pruned middle: fp32 shadow rows + quad minima, two bulk copies "
                               "per ring stage; coarse bounds from the quad minima, per-cell exact lower-bound "
                               "filter; fired splits handed to the sub-product)",
