@@ -124,6 +124,19 @@ int rotor_solve_device(const rotor_chain *d_chain, int32_t L, uint64_t mem_limit
 /* Device workspace bytes needed for (L, S, options). */
 int rotor_workspace_bytes(int32_t L, int32_t slots, const rotor_options *opt, uint64_t *bytes);
 
+/* Test / debug aid: where the tiled fill keeps its fp32 round-down shadows in
+ * a workspace of rotor_workspace_bytes, so a caller holding
+ * the workspace (rotor_solve_device) can check them against the fp64 table.
+ * out[0] byte offset of C32, out[1] rows of C32 (scrows), out[2] byte offset
+ * of A32, out[3] rows of A32 (sarows), out[4] byte offset of C (the cell
+ * (1,1) at m = 0), out[5] doubles per C row (pitch).  C32 / A32 are float
+ * arrays in the m-chunked layout: element (row, m) at ((m / 32) * rows + row)
+ * * 32 + m % 32; rows follow srow_c / srow_a / sc_row / sa_col of
+ * rotor_common.cuh (block-major, 32 cells then 8 quad minima per block
+ * column / row).  Shadows exist only for the tiled kernel (ROTOR_EINPUT for
+ * an options set without them). */
+int rotor_shadow_layout(int32_t L, int32_t slots, const rotor_options *opt, int64_t out[6]);
+
 /* Upper bound on the op count of any schedule Algorithm 2 can return for L:
  * n(n+1)/2 forwards + n backwards, n = L+1 (a node (s,t) split at s' emits
  * s'-s forwards; by induction an interval of len stages emits at most

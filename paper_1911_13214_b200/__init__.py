@@ -82,6 +82,7 @@ _lib.rotor_solve_ex.argtypes = [_P(rotor_chain), _i32, _u64, _i32, _P(rotor_opti
 _lib.rotor_solve_device.argtypes = [_P(rotor_chain), _i32, _u64, _i32, _P(rotor_options), _vp, _u64, _vp, _vp, _vp,
                                     _i64, _vp, _vp]
 _lib.rotor_workspace_bytes.argtypes = [_i32, _i32, _P(rotor_options), _P(_u64)]
+_lib.rotor_shadow_layout.argtypes = [_i32, _i32, _P(rotor_options), _P(_i64)]
 _lib.rotor_max_ops.argtypes = [_i32]
 _lib.rotor_max_ops.restype = _i64
 _lib.rotor_solve_batch.argtypes = [_P(rotor_chain), _P(_i32), _i32, _P(_u64), _i32, _i32, _P(rotor_options), _P(_i32),
@@ -110,7 +111,8 @@ _lib.rotor_version.restype = _i32
 
 # every symbol include/rotor.h declares (checked by tests/test_abi.py)
 EXPORTS = (
-    "rotor_solve", "rotor_solve_ex", "rotor_solve_device", "rotor_workspace_bytes", "rotor_max_ops",
+    "rotor_solve", "rotor_solve_ex", "rotor_solve_device", "rotor_workspace_bytes", "rotor_shadow_layout",
+    "rotor_max_ops",
     "rotor_solve_batch", "rotor_solve_sharded", "rotor_partition_lpt", "rotor_transitions", "rotor_export_tables", "rotor_export_rows",
     "rotor_last_timings", "rotor_last_counters",
     "rotor_release", "rotor_last_error", "rotor_version",
@@ -233,6 +235,14 @@ def _ws(workspace):
     if workspace is None:
         return None, 0
     return int(workspace.data_ptr()), int(workspace.numel() * workspace.element_size())
+
+
+def shadow_layout(L: int, slots: int, **opts) -> dict:
+    """rotor_shadow_layout: byte offsets / row counts of the tiled fill's fp32 shadows in a workspace."""
+    arr = (_i64 * 6)()
+    o = _options(**opts)
+    _check(_lib.rotor_shadow_layout(int(L), int(slots), _c.byref(o), arr))
+    return dict(c32_off=arr[0], c32_rows=arr[1], a32_off=arr[2], a32_rows=arr[3], c_off=arr[4], pitch=arr[5])
 
 
 def solve_device(d_chain: dict, L: int, mem_limit: int, slots: int, workspace, out: dict, stream=None, **opts) -> int:

@@ -583,6 +583,21 @@ int rotor_workspace_bytes(int32_t L, int32_t slots, const rotor_options *opt, ui
     return ROTOR_OK;
 }
 
+int rotor_shadow_layout(int32_t L, int32_t slots, const rotor_options *opt, int64_t out[6]) {
+    int r = check_args(L, 1, slots);
+    if (r) return r;
+    if (!out) return fail(ROTOR_EINPUT, "out is NULL");
+    const Layout y = make_layout(L, slots, opts_or_default(opt));
+    if (!y.has_A) return fail(ROTOR_EINPUT, "these options use no shadows (not the tiled kernel)");
+    out[0] = (int64_t)y.off_C32;
+    out[1] = y.scrows;
+    out[2] = (int64_t)y.off_A32;
+    out[3] = y.sarows;
+    out[4] = (int64_t)y.off_C + (int64_t)rotor::kPad * 8;
+    out[5] = y.pitch;
+    return ROTOR_OK;
+}
+
 int rotor_solve_device(const rotor_chain *d_chain, int32_t L, uint64_t mem_limit, int32_t slots,
                        const rotor_options *opt, void *d_workspace, uint64_t workspace_bytes, void *stream,
                        double *d_cost, rotor_op *d_ops, int64_t ops_cap, int64_t *d_n_ops, int32_t *d_status) {
