@@ -318,6 +318,15 @@ typedef struct {
     uint64_t middle_flush_cycles;   /* the exact fp64 pass of the fired splits */
     double middle_warp_imbalance;   /* max / mean over the 16 warp slots of (loop + flush) cycles */
     uint64_t middle_slot_cycles[16];/* (loop + flush) cycles per warp slot = 8 x 8 sub-tile position in the tile */
+    /* where the off-diagonal leaves' time goes (ns of GPU global timer, summed
+     * over CTAs, thread 0 of each): setup (arrival ticket, sub-tile tables,
+     * staged operands), waiting for the lower m-chunks' rows (look-back
+     * flags), the rows' own work, the per-row barrier + release */
+    uint64_t leaf_ctas;
+    uint64_t leaf_setup_ns;
+    uint64_t leaf_wait_ns;
+    uint64_t leaf_work_ns;
+    uint64_t leaf_sync_ns;
 } rotor_counters;
 int rotor_last_counters(rotor_counters *out);
 

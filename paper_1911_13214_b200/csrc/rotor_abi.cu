@@ -1267,7 +1267,7 @@ int rotor_last_counters(rotor_counters *out) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
     if (dev != g_last.device) CK(cudaSetDevice(g_last.device));
-    unsigned long long c[8 + 16];
+    unsigned long long c[32];
     CK(cudaStreamSynchronize(g_last.stream));
     CK(cudaMemcpy(c, g_last.p.counters, sizeof c, cudaMemcpyDeviceToHost));
     if (dev != g_last.device) CK(cudaSetDevice(dev));
@@ -1291,6 +1291,11 @@ int rotor_last_counters(rotor_counters *out) {
         out->middle_slot_cycles[w] = c[8 + w];
     }
     out->middle_warp_imbalance = sum ? mx * 16.0 / (double)sum : 0.0;
+    out->leaf_ctas = c[24];
+    out->leaf_setup_ns = c[25];
+    out->leaf_wait_ns = c[26];
+    out->leaf_work_ns = c[27];
+    out->leaf_sync_ns = c[28];
     return ROTOR_OK;
 }
 

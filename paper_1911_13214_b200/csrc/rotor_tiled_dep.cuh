@@ -44,6 +44,11 @@ __host__ __device__ inline void sub_at(int delta, int e, int q, int &alpha, int 
 // tile diagonal (another CTA, earlier kernel of this Delta) -> L2 (.cg);
 // otherwise written by an earlier tile diagonal -> plain (L1-cacheable).
 __device__ __forceinline__ double ld(const double *p, bool fresh) { return fresh ? __ldcg(p) : *p; }
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 constexpr int PH = SB / 2;  // columns per product lane
 
@@ -531,7 +536,7 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
 // RS: the right-range operands R[c][cq] = C(t0+cq, t0+c, m - wx[t0+cq-1]),
 // the same for every row, are loaded once into shared memory (thread-private
 // columns, NPAIR x LEAF_M doubles) instead of once per row.
-template <bool RS>
+template <bool RS, bool TIMED = false>
 __global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS) k_sub_leaf_row(Problem p, int delta, int e, int *flags,
                                                                         int phase_id, int tile_lo, unsigned *ticket) {
     __shared__ LeafTab T;
@@ -539,6 +544,11 @@ __global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS)
     const int n = p.n;
     const int n_chunks = (p.S + 1 + LEAF_M - 1) / LEAF_M;
     const int cnt = sub_count(delta, e);
+    // time split (options.counters; thread 0, global timer): setup / look-back
+    // wait / row work / barrier + release, summed into counters 24..28
+    constexpr bool timed = TIMED;  // (the counters solve only: the timing state costs registers)
+    unsigned long long tm0 = 0, t_wait = 0, t_work = 0, t_sync = 0;
+    if (timed && threadIdx.x == 0) tm0 = gtimer();
     const int bid = leaf_ticket(ticket);  // before any early exit: every CTA draws one
     const int q = bid % n_chunks;
     const int sub = bid / n_chunks;
@@ -571,9 +581,19 @@ __global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS)
     float qa[SB];  // quad minima of the columns over the current 4-row group
 #pragma unroll
     for (int c = 0; c < SB; c++) qa[c] = INFINITY;
+    unsigned long long tm = (timed && threadIdx.x == 0) ? gtimer() : 0;
+    const unsigned long long t_setup = tm - tm0;
+    auto lap = [&](unsigned long long &acc) {
+        if (timed && threadIdx.x == 0) {
+            const unsigned long long x = gtimer();
+            acc += x - tm;
+            tm = x;
+        }
+    };
 #pragma unroll
     for (int r = SB - 1; r >= 0; r--) {
         auto wait = [&]() {  // uniform over the CTA (every thread calls it once per row)
+            lap(t_work);
             if (r == SB - 1) return;
             const int need = (phase_id << 4) | (SB - 1 - r);  // rows SB-1 .. r+1 done
             for (int qq = q_lo + (int)threadIdx.x; qq < q; qq += LEAF_M) {
@@ -583,6 +603,7 @@ __global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS)
                 } while (v < need);
             }
             __syncthreads();
+            lap(t_wait);
         };
         const bool live = m <= p.S;
         if (s0 + r > n) {  // no such row (uniform)
@@ -607,10 +628,19 @@ __global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS)
                 qa[c] = INFINITY;
             }
         }
+        lap(t_work);
         __syncthreads();
         if (threadIdx.x == 0)
             asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(my_flags + q), "r"((phase_id << 4) | (SB - r))
                          : "memory");
+        lap(t_sync);
+    }
+    if (timed && threadIdx.x == 0) {
+        atomicAdd(p.counters + 24, 1ull);
+        atomicAdd(p.counters + 25, t_setup);
+        atomicAdd(p.counters + 26, t_wait);
+        atomicAdd(p.counters + 27, t_work);
+        atomicAdd(p.counters + 28, t_sync);
     }
 }
 
@@ -694,6 +724,9 @@ inline int launch_dependent(const Problem &p, int delta, int tile_lo, int tile_h
         unsigned *ticket = reinterpret_cast<unsigned *>(flags + leaf_flag_words(p.L, p.S)) + tile_lo;
         if (delta == 0 && e == 0)
             k_sub_leaf_diag<<<lb, LEAF_M, 0, st>>>(p, delta, e, flags, ++phase_id, tile_lo, ticket);
+        else if (leaf_staged() && p.counters)
+            k_sub_leaf_row<true, true><<<lb, LEAF_M, NPAIR * LEAF_M * 8, st>>>(p, delta, e, flags, ++phase_id, tile_lo,
+                                                                                ticket);
         else if (leaf_staged())
             k_sub_leaf_row<true><<<lb, LEAF_M, NPAIR * LEAF_M * 8, st>>>(p, delta, e, flags, ++phase_id, tile_lo, ticket);
         else
