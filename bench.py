@@ -713,7 +713,7 @@ def run_ours(args):
             "middle_slot_cycles": c["middle_slot_cycles"],
             # off-diagonal leaves: per CTA, where its lifetime goes (us, global timer, thread 0)
             "leaf_time_split_us_per_cta": ({k: c[f"leaf_{k}_ns"] / 1e3 / c["leaf_ctas"]
-                                            for k in ("setup", "wait", "work", "sync")} | {"ctas": c["leaf_ctas"]})
+                                            for k in ("setup", "wait", "pass1", "work", "sync")} | {"ctas": c["leaf_ctas"]})
                                            if c.get("leaf_ctas") else None,
             "note": "value counts NOMINAL transitions (every cell of diagonal d: d + 1 candidates, Eq. 2); "
                     "evaluated = fp32 filter compares + fp64 exact candidates of the pruned middle + every "

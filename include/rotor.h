@@ -325,8 +325,9 @@ typedef struct {
     uint64_t leaf_ctas;
     uint64_t leaf_setup_ns;
     uint64_t leaf_wait_ns;
-    uint64_t leaf_work_ns;
+    uint64_t leaf_work_ns;          /* the rows after pass 1: right range, F_all, stores (+ the next row's early loads) */
     uint64_t leaf_sync_ns;
+    uint64_t leaf_pass1_ns;         /* the rows' pass 1: the rows-below / F_all loads and the left range */
 } rotor_counters;
 int rotor_last_counters(rotor_counters *out);
 

@@ -69,7 +69,7 @@ class rotor_counters(ctypes.Structure):
         ("middle_loop_cycles", ctypes.c_uint64), ("middle_flush_cycles", ctypes.c_uint64),
         ("middle_warp_imbalance", ctypes.c_double), ("middle_slot_cycles", ctypes.c_uint64 * 16),
         ("leaf_ctas", ctypes.c_uint64), ("leaf_setup_ns", ctypes.c_uint64), ("leaf_wait_ns", ctypes.c_uint64),
-        ("leaf_work_ns", ctypes.c_uint64), ("leaf_sync_ns", ctypes.c_uint64),
+        ("leaf_work_ns", ctypes.c_uint64), ("leaf_sync_ns", ctypes.c_uint64), ("leaf_pass1_ns", ctypes.c_uint64),
     ]
 
 

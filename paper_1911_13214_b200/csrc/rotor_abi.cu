@@ -1296,6 +1296,7 @@ int rotor_last_counters(rotor_counters *out) {
     out->leaf_wait_ns = c[26];
     out->leaf_work_ns = c[27];
     out->leaf_sync_ns = c[28];
+    out->leaf_pass1_ns = c[29];
     return ROTOR_OK;
 }
 

@@ -424,9 +424,10 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
 // code, measured slower in the tile-DAG schedule too: 143.2 vs 131.1 ms per solve)
 // qa: the running quad minima of the sub-tile's columns over the rows of the
 // current 4-row group (k_sub_leaf_row writes them after rows 4 and 0).
-template <int r, bool RS, class Wait>
+template <int r, bool RS, class Wait, class Lap>
 __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T, bool fresh, bool partial, int s0,
-                                             int t0, int m, bool live, const double *Rs, float (&qa)[SB], Wait wait) {
+                                             int t0, int m, bool live, const double *Rs, float (&qa)[SB], Wait wait,
+                                             Lap after_pass1) {
     const int n = p.n;
     const int64_t pitch = p.pitch;
     const int s = s0 + r;
@@ -466,6 +467,7 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
         B[c] = best;
         F[c] = m >= T.mall[r][c] ? __dadd_rn(T.w[r], __ldcg(Cm + T.crow[r + 1] + c * pitch - T.wbx[r])) : INFINITY;
     }
+    after_pass1();               // (timing only)
     if (RS) cp_async_wait<0>();  // this thread's right-range operands are in shared memory
     // the row's outputs, addressed incrementally: cells (s, t0+c) are consecutive
     // C rows, and consecutive C32 shadow rows (pre-shifted by wx[s-1]) followed
@@ -547,7 +549,7 @@ __global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS)
     // time split (options.counters; thread 0, global timer): setup / look-back
     // wait / row work / barrier + release, summed into counters 24..28
     constexpr bool timed = TIMED;  // (the counters solve only: the timing state costs registers)
-    unsigned long long tm0 = 0, t_wait = 0, t_work = 0, t_sync = 0;
+    unsigned long long tm0 = 0, t_wait = 0, t_work = 0, t_sync = 0, t_pass1 = 0;
     if (timed && threadIdx.x == 0) tm0 = gtimer();
     const int bid = leaf_ticket(ticket);  // before any early exit: every CTA draws one
     const int q = bid % n_chunks;
@@ -605,19 +607,20 @@ __global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS)
             __syncthreads();
             lap(t_wait);
         };
+        auto pass1 = [&]() { lap(t_pass1); };
         const bool live = m <= p.S;
         if (s0 + r > n) {  // no such row (uniform)
             wait();
         } else {
             switch (r) {  // compile-time row index: the row's loops fully unrolled
-                case 0: leaf_row_tab<0, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
-                case 1: leaf_row_tab<1, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
-                case 2: leaf_row_tab<2, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
-                case 3: leaf_row_tab<3, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
-                case 4: leaf_row_tab<4, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
-                case 5: leaf_row_tab<5, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
-                case 6: leaf_row_tab<6, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
-                default: leaf_row_tab<7, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait); break;
+                case 0: leaf_row_tab<0, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait, pass1); break;
+                case 1: leaf_row_tab<1, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait, pass1); break;
+                case 2: leaf_row_tab<2, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait, pass1); break;
+                case 3: leaf_row_tab<3, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait, pass1); break;
+                case 4: leaf_row_tab<4, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait, pass1); break;
+                case 5: leaf_row_tab<5, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait, pass1); break;
+                case 6: leaf_row_tab<6, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait, pass1); break;
+                default: leaf_row_tab<7, RS>(p, T, fresh, partial, s0, t0, m, live, Rsm, qa, wait, pass1); break;
             }
         }
         if ((r & 3) == 0 && live) {  // rows r..r+3 done: the columns' quad minima (A(s, t) exists for t < n)
@@ -641,6 +644,7 @@ __global__ void __launch_bounds__(LEAF_M, RS ? LEAF_RS_BLOCKS : LEAF_MIN_BLOCKS)
         atomicAdd(p.counters + 26, t_wait);
         atomicAdd(p.counters + 27, t_work);
         atomicAdd(p.counters + 28, t_sync);
+        atomicAdd(p.counters + 29, t_pass1);
     }
 }
 
