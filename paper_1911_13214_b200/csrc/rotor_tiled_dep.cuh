@@ -379,6 +379,8 @@ struct LeafTab {
     double wd[SB];                    // w[t0+c]: its value (Eq. 1)
     double w[SB], Ps[SB], Pt[SB];     // w[s0+r], P[s0+r-1], P[t0+c]
     int64_t crow[SB + 1];             // element offset of C cell (s0+j, t0) (columns t0+c follow, pitch apart)
+    int64_t cleft[SB];                // crow[j] - wxl[j]: the left split s' = s0+j's operand row, shifted
+    int64_t cfall[SB];                // crow[r+1] - wbx[r]: row r's F_all operand row, shifted
     int64_t arow[SB];                 // element offset of A(s0+r, t0-1)
     int64_t aleft[SB][SB - 1];        // element offset of A(s0+r, s0+r+k) (left split s' = s0+r+k+1)
     int q_lo;                         // lowest m-chunk a shifted read of a row below can reach
@@ -413,6 +415,10 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
         int wmax = 0;
         for (int k = 0; k < SB; k++) wmax = max(wmax, max(T.wxl[k], T.wbx[k]));
         T.q_lo = m0 - wmax <= 0 ? 0 : (m0 - wmax) / chunk_m;
+    } else if (threadIdx.x <= SB) {  // one 64-bit offset per operand row instead of two loads + an add per candidate
+        const int k = threadIdx.x - 1;
+        T.cleft[k] = T.crow[k] - T.wxl[k];
+        T.cfall[k] = T.crow[k + 1] - T.wbx[k];
     }
     __syncthreads();
 }
@@ -460,12 +466,12 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
             for (int k = 0; k < SB - 1; k++) {  // left: C of the rows below in this sub-tile
                 if (k >= SB - 1 - r) break;
                 const int j = r + k + 1;  // s' = s0 + j
-                const double cv = __ldcg(Cm + T.crow[j] + c * pitch - T.wxl[j]);
+                const double cv = __ldcg(Cm + T.cleft[j] + c * pitch);
                 best = dmin(best, __dadd_rn(AL[k], cv));
             }
         }
         B[c] = best;
-        F[c] = m >= T.mall[r][c] ? __dadd_rn(T.w[r], __ldcg(Cm + T.crow[r + 1] + c * pitch - T.wbx[r])) : INFINITY;
+        F[c] = m >= T.mall[r][c] ? __dadd_rn(T.w[r], __ldcg(Cm + T.cfall[r] + c * pitch)) : INFINITY;
     }
     after_pass1();               // (timing only)
     if (RS) cp_async_wait<0>();  // this thread's right-range operands are in shared memory
