@@ -379,8 +379,8 @@ struct LeafTab {
     double wd[SB];                    // w[t0+c]: its value (Eq. 1)
     double w[SB], Ps[SB], Pt[SB];     // w[s0+r], P[s0+r-1], P[t0+c]
     int64_t crow[SB + 1];             // element offset of C cell (s0+j, t0) (columns t0+c follow, pitch apart)
-    int64_t cleft[SB];                // crow[j] - wxl[j]: the left split s' = s0+j's operand row, shifted
-    int64_t cfall[SB];                // crow[r+1] - wbx[r]: row r's F_all operand row, shifted
+    int64_t cleft[SB];                // 8 (crow[j] - wxl[j]): byte offset of the left split s' = s0+j's operand row, shifted
+    int64_t cfall[SB];                // 8 (crow[r+1] - wbx[r]): byte offset of row r's F_all operand row, shifted
     int64_t arow[SB];                 // element offset of A(s0+r, t0-1)
     int64_t aleft[SB][SB - 1];        // element offset of A(s0+r, s0+r+k) (left split s' = s0+r+k+1)
     int q_lo;                         // lowest m-chunk a shifted read of a row below can reach
@@ -417,8 +417,8 @@ __device__ __forceinline__ void leaf_tab_fill(const Problem &p, int s0, int t0, 
         T.q_lo = m0 - wmax <= 0 ? 0 : (m0 - wmax) / chunk_m;
     } else if (threadIdx.x <= SB) {  // one 64-bit offset per operand row instead of two loads + an add per candidate
         const int k = threadIdx.x - 1;
-        T.cleft[k] = T.crow[k] - T.wxl[k];
-        T.cfall[k] = T.crow[k + 1] - T.wbx[k];
+        T.cleft[k] = (T.crow[k] - T.wxl[k]) * 8;
+        T.cfall[k] = (T.crow[k + 1] - T.wbx[k]) * 8;
     }
     __syncthreads();
 }
@@ -451,13 +451,22 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     double B[SB], F[SB];
     bool gate[SB];
     const int64_t crow = T.crow[r];
+    {
+        const double *pb = Cm + crow;
 #pragma unroll
-    for (int c = 0; c < SB; c++) {
-        gate[c] = live && m >= T.mnull[r][c];  // INT_MAX past the last stage
-        B[c] = (gate[c] && partial) ? __ldcg(Cm + crow + c * pitch) : INFINITY;
+        for (int c = 0; c < SB; c++) {
+            gate[c] = live && m >= T.mnull[r][c];  // INT_MAX past the last stage
+            B[c] = (gate[c] && partial) ? __ldcg(pb) : INFINITY;
+            pb += pitch;
+        }
     }
     wait();  // the rows below are complete at every m this row reads (flags + barrier)
     if (!live) return;
+    // byte addressing with a running column pointer: per candidate one
+    // shared-memory offset, one 64-bit add and the load (the element-index form
+    // recomputed pitch * c and scaled for every load)
+    const char *colb = reinterpret_cast<const char *>(Cm);
+    const int64_t pitch_b = pitch * 8;
 #pragma unroll
     for (int c = 0; c < SB; c++) {
         double best = B[c];
@@ -466,12 +475,14 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
             for (int k = 0; k < SB - 1; k++) {  // left: C of the rows below in this sub-tile
                 if (k >= SB - 1 - r) break;
                 const int j = r + k + 1;  // s' = s0 + j
-                const double cv = __ldcg(Cm + T.cleft[j] + c * pitch);
+                const double cv = __ldcg(reinterpret_cast<const double *>(colb + T.cleft[j]));
                 best = dmin(best, __dadd_rn(AL[k], cv));
             }
         }
         B[c] = best;
-        F[c] = m >= T.mall[r][c] ? __dadd_rn(T.w[r], __ldcg(Cm + T.cfall[r] + c * pitch)) : INFINITY;
+        F[c] = m >= T.mall[r][c] ? __dadd_rn(T.w[r], __ldcg(reinterpret_cast<const double *>(colb + T.cfall[r])))
+                                 : INFINITY;
+        colb += pitch_b;
     }
     after_pass1();               // (timing only)
     if (RS) cp_async_wait<0>();  // this thread's right-range operands are in shared memory
@@ -488,8 +499,12 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
     float *q32_hi = (m + w <= p.S) ? p.C32 + shadow_index(p.scrows, q_row32, m + w) : nullptr;
     float *q32_lo = (m < w) ? p.C32 + shadow_index(p.scrows, q_row32, m) : nullptr;
     float qc[2] = {INFINITY, INFINITY};
-    int64_t a_row = a_index(s, t0);
-    int64_t a_row32 = srow_a(n, s, t0);
+    // running output pointers: C(s, t) -> C(s, t+1) one row, A(s, t) -> A(s, t+1)
+    // t rows (a_index), A32 kSR shadow rows = kSR * kSW floats
+    double *pc = Cm + crow;
+    double *pa = p.A + a_index(s, t0) * pitch + m;
+    int64_t a_step = (int64_t)t0 * pitch;
+    float *pa32 = p.A32 + shadow_index(p.sarows, srow_a(n, s, t0), m);
 #pragma unroll
     for (int c = 0; c < SB; c++) {
         const int t = t0 + c;
@@ -511,7 +526,8 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
             c1 = best;
         }
         const double cc = dmin(c1, F[c]);
-        Cm[crow + c * pitch] = cc;  // store_final_c, unrolled
+        *pc = cc;  // store_final_c, unrolled
+        pc += pitch;
         const float c32 = __double2float_rd(cc);
         if (c32_hi) c32_hi[c * kSW] = c32;
         if (c32_lo) c32_lo[c * kSW] = INFINITY;
@@ -519,12 +535,13 @@ __device__ __forceinline__ void leaf_row_tab(const Problem &p, const LeafTab &T,
         const double a = __dadd_rn(__dadd_rn(T.Pt[c], -T.Ps[r]), cc);
         if (t < n) {  // store_final_a
             const float a32 = __double2float_rd(a);
-            p.A[a_row * pitch + m] = a;
-            p.A32[shadow_index(p.sarows, a_row32, m)] = a32;
+            *pa = a;
+            *pa32 = a32;
             qa[c] = fminf(qa[c], a32);
         }
-        a_row += t;
-        a_row32 += kSR;
+        pa += a_step;
+        a_step += pitch;
+        pa32 += kSR * kSW;
         AR[c + 1] = a;
     }
     // the row's two column-group minima (a group with no cell: +inf)
