@@ -77,7 +77,12 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int MINB>
 __global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product_async(Problem p, int delta, int e, int tile_lo,
                                                                          int ntiles) {
-    __shared__ int wxs[PW][2 * TB];
+    // per warp and split: the element offsets of its operand rows A(s0, s'-1)
+    // and C(s', t0) (shifted by -w) and its shift w, computed once by the
+    // warp's lanes in parallel (each lane's own rows / m are a constant offset)
+    constexpr int NSPMAX = 2 * (TB - SB) + MLIST_CAP + 1;
+    __shared__ long long soff[PW][NSPMAX][2];
+    __shared__ int sw[PW][NSPMAX];
     __shared__ double ring[PW][PNS][2][SB][16];  // [warp][stage][A | C][row | column][m]
     const int n = p.n, S = p.S;
     const int cnt = sub_count(delta, e);
@@ -121,65 +126,45 @@ __global__ void __launch_bounds__(DEP_THREADS, MINB) k_sub_product_async(Problem
     const int n1 = max(0, hi1 - lo1 + 1), n2 = max(0, hi2 - lo2 + 1), nsp = n1 + n2 + n3;
     if (s0 > n || t0 > n) return;      // no cells (uniform over the warp)
     if (nsp == 0 && (!partial || mid_partial)) return;  // nothing to add; the partial (if any) is final
-    int *ws = wxs[wid];
-    if (lane < n1) ws[lane] = p.wx[lo1 + lane - 1];
-    if (lane < n2) ws[TB + lane] = p.wx[lo2 + lane - 1];
-    __syncwarp();
     const int64_t pitch = p.pitch;
     const bool mlive = m <= S;
     const int sp_mid = i0 + TB;  // s' of middle split index 0
-    // split idx: 0..n1-1 -> s' = lo1 + idx (left), n1.. -> s' = lo2 + idx - n1 (right).
-    // Issued in order, so the lane walks its operand rows incrementally: rows
-    // s0+jh.. of A column q-1 and cells (q, t0+jh..) are consecutive table rows,
-    // A column q-1 -> q moves a_index by q-1 rows, cell (q,t) -> (q+1,t) moves
-    // cell_index by n-q rows (s-major).
+    // split idx: 0..n1-1 -> s' = lo1 + idx (left), n1..n1+n2-1 -> s' = lo2 + idx - n1
+    // (right), then the middle's recorded splits s' = sp_mid + lst[1 + ...]
+    for (int idx = lane; idx < nsp; idx += 32) {
+        const int sp = idx < n1 ? lo1 + idx : (idx < n1 + n2 ? lo2 + idx - n1 : sp_mid + lst[1 + idx - n1 - n2]);
+        const int w = p.wx[sp - 1];
+        soff[wid][idx][0] = a_index(s0, sp - 1) * pitch;
+        soff[wid][idx][1] = cell_index(n, sp, t0) * pitch - w;
+        sw[wid][idx] = w;
+    }
+    __syncwarp();
+    // rows s0+jh.. of an A column and cells (s', t0+jh..) are consecutive table rows
     const int64_t pitch4[PH] = {0, pitch, 2 * pitch, 3 * pitch};
+    const int64_t lane_off = (int64_t)jh * pitch + m;
     unsigned rows_a = 0, rows_c = 0;  // which of the lane's rows / columns exist
 #pragma unroll
     for (int i = 0; i < PH; i++) {
         rows_a |= (s0 + jh + i <= n) << i;
         rows_c |= (t0 + jh + i <= n) << i;
     }
-    int nx = 0, q = n1 > 0 ? lo1 : (n2 > 0 ? lo2 : sp_mid);
-    const double *pa = p.A + a_index(s0 + jh, q - 1) * pitch + m;
-    const double *pc = p.C + cell_index(n, q, t0 + jh) * pitch + m;
+    int nx = 0;
     auto issue_next = [&]() {
         double(*st)[SB][16] = ring[wid][nx % PNS];
-        if (nx >= n1 + n2) {  // a split the middle recorded: addresses computed directly
-            const int sp = sp_mid + lst[1 + nx - n1 - n2];
-            const int w = p.wx[sp - 1];
-            const bool use = mlive && m >= w;
-            const double *la = p.A + a_index(s0 + jh, sp - 1) * pitch + m;
-            const double *lc = p.C + cell_index(n, sp, t0 + jh) * pitch + (use ? m - w : m);
-#pragma unroll
-            for (int i = 0; i < PH; i++) {
-                cp_async8_zfill(&st[0][jh + i][mi], la + pitch4[i], use && ((rows_a >> i) & 1));
-                cp_async8_zfill(&st[1][jh + i][mi], lc + pitch4[i], use && ((rows_c >> i) & 1));
-            }
-            ++nx;
-            return;
-        }
-        const int w = nx < n1 ? ws[nx] : ws[TB + nx - n1];
+        const int w = sw[wid][nx];
         // A skipped operand is zero-filled: m < w means every cell the split
         // feeds is gated (m < w <= m_null, DESIGN Q6), so its partial is never
         // read; a row / column past the last stage feeds only cells that do not
         // exist.  Branch-free copies (src-size 0 reads nothing).
         const bool use = mlive && m >= w;
-        const double *pcw = use ? pc - w : pc;
+        const double *la = p.A + soff[wid][nx][0] + lane_off;
+        const double *lc = p.C + soff[wid][nx][1] + lane_off + (use ? 0 : w);
 #pragma unroll
         for (int i = 0; i < PH; i++) {
-            cp_async8_zfill(&st[0][jh + i][mi], pa + pitch4[i], use && ((rows_a >> i) & 1));
-            cp_async8_zfill(&st[1][jh + i][mi], pcw + pitch4[i], use && ((rows_c >> i) & 1));
+            cp_async8_zfill(&st[0][jh + i][mi], la + pitch4[i], use && ((rows_a >> i) & 1));
+            cp_async8_zfill(&st[1][jh + i][mi], lc + pitch4[i], use && ((rows_c >> i) & 1));
         }
-        if (++nx == n1 && n2 > 0) {  // on to the right range
-            q = lo2;
-            pa = p.A + a_index(s0 + jh, q - 1) * pitch + m;
-            pc = p.C + cell_index(n, q, t0 + jh) * pitch + m;
-        } else {
-            pa += (int64_t)(q - 1) * pitch;
-            pc += (int64_t)(n - q) * pitch;
-            q++;
-        }
+        ++nx;
     };
     // the lane's cells (s0+i, t0+jh+j): row i starts cell_index(n, s0+i, t0+jh),
     // rows s -> s+1 are n-s cells apart (s-major), columns consecutive
