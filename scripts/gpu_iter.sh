@@ -2,7 +2,7 @@
 # One build -> measure iteration on the GPU box: a parity subset, then short
 # benches of the env-selected variants (VAR / VALUES), then old-vs-new A/B
 # against abtest/ when it exists.
-# Usage: PYTEST_K="tiled" VAR=ROTOR_WRING VALUES="44 46" bash scripts/gpu_iter.sh <tag>
+# Usage: PYTEST_K="tiled" VAR=ROTOR_WRING VALUES="82 44" bash scripts/gpu_iter.sh <tag>
 set -u
 TAG=${1:-it}; OUT=gpurun_out/$TAG; mkdir -p "$OUT"
 python -c "import __graft_entry__ as g; g.build()" > "$OUT/build.log" 2>&1 || { tail -30 "$OUT/build.log"; exit 1; }
