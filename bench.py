@@ -410,7 +410,6 @@ def run_batched(args):
         tot, tot_bytes = float(c[0].item()), float(c[1].item())
         sec = float(t.item()) / 1e3
         peaks, peak_kind = measured_peaks()
-        achieved = tot_bytes * args.steps / sec / 1e9
         peak = float(peaks["hbm_gbs"]) * world
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -436,6 +435,7 @@ def run_batched(args):
                     kb_traffic = json.load(f)["k_batch"]["dram_bytes_per_launch"]
             except Exception:
                 kb_traffic = None
+        achieved = kb_traffic * args.steps / sec / 1e9 if kb_traffic else None
         line = {"metric": "DP cell-transitions/sec, batched 256-limit x 8-chain sweep (config 5)",
                 "value": tot * args.steps / sec, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": float(t.item()) / args.steps,
@@ -445,12 +445,16 @@ def run_batched(args):
                                                  "note": "host-buffer API: H2D chains/limits and D2H costs+ops inside the timed region"},
                 "clocks": clk,
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": kb_traffic, "peak_source": peak_kind,
-                             "traffic_over_alg": (kb_traffic / tot_bytes) if kb_traffic else None,
+                             "frac": achieved / peak if achieved is not None else None,
+                             "traffic": kb_traffic, "peak_source": peak_kind,
+                             "model": "measured_dram_bytes: the pruned k_batch skips candidates by a data-dependent "
+                                      "bound (DESIGN 5.3), so its bytes have no closed form; achieved = the launch's "
+                                      "ncu DRAM read+write bytes / the live step time (null for N > 1)",
                              "traffic_scope": "DRAM read+write bytes of the one k_batch launch of a step, one ncu "
                                               "--set full capture (profiles/ncu_summary.json k_batch); null for N > 1",
-                             "kernel": "k_batch (fused: discretise, limits, wavefront fill, Algorithm 2 per table)",
-                             "alg_bytes_per_step": tot_bytes},
+                             "kernel": "k_batch (fused: discretise, limits, pruned wavefront fill, Algorithm 2 per table)",
+                             "wavefront_alg_bytes_per_step": tot_bytes,
+                             "speedup_vs_wavefront_roofline": tot_bytes * args.steps / (peak * 1e9) / sec},
                 "cpu_baseline": cpu, "gpu_launches": args.steps * world}
         print(json.dumps(line), flush=True)
     if pg:

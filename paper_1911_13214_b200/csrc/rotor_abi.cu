@@ -441,11 +441,11 @@ int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind
     for (int64_t k = 0; k < P; k++) h_order[k] = (int32_t)k;
     std::stable_sort(h_order.begin(), h_order.end(),
                      [&](int32_t x, int32_t y) { return in.Ls[h_pc[x]] > in.Ls[h_pc[y]]; });
-    // persistent k_batch CTAs (512 threads, 32 registers): four resident per SM,
-    // a full SM of threads (config 5: 1 per SM 86.4 ms, 2 59.0, 3 50.0 at 40
+    // persistent k_batch CTAs (512 threads): batch_ctas_per_sm() resident per SM
+    // (rotor_batch.cu; before the pruning, config 5: 1 per SM 86.4 ms, 2 59.0, 3 50.0 at 40
     // registers / 47.5 at 32, 4 44.6; 256 threads x 6 62.6, x 7 60.6; 384 x 4
     // 50.6; 128 x 12 91.2)
-    const int n_slots = (int)std::min<int64_t>(P, 4 * (int64_t)sms);
+    const int n_slots = (int)std::min<int64_t>(P, rotor::batch_ctas_per_sm() * (int64_t)sms);
     const size_t slot = rotor::batch_slot_bytes(L_max, slots);
     // one device allocation (a leased library workspace): descriptors, outputs, ops, then the slot pool
     size_t off = 0;
@@ -498,13 +498,22 @@ int batch_on_device(const BatchIn &in, const std::vector<int64_t> &idx, int kind
     b.ops_cap = (const int64_t *)(w + o_cap);
     b.counter = (int *)(w + o_ctr);
     b.order = (const int32_t *)(w + o_ord);
-    // ROTOR_BATCH_MC: m-chunk of k_batch's fill order (config 5, ms per sweep:
-    // whole rows 31.6, 16 m 31.8, 32 m 32.7, 64 m 30.8, 128 m 29.2)
+    // ROTOR_BATCH_MC: m-chunk of k_batch's fill order (config 5, ms per sweep,
+    // every candidate: whole rows 31.6, 16 m 31.8, 32 m 32.7, 64 m 30.8, 128 m
+    // 29.2; pruned: whole rows 26.9, 64 m 18.5, 128 m 19.6, 256 m 21.3)
     static const int batch_mc = [] {
         const char *e = getenv("ROTOR_BATCH_MC");
-        return e ? atoi(e) : 128;
+        return e ? atoi(e) : 64;
     }();
     b.mc = batch_mc;
+    // ROTOR_BATCH_PRUNE: 1 (default) the monotone-in-m bound per warp of 32 m,
+    // 2/4 per 16/8 m (config 5: 18.9 / 22.3 / 23.4 ms), 0 every candidate of
+    // every cell (wavefront_cell, 26.2 ms)
+    static const int batch_prune = [] {
+        const char *e = getenv("ROTOR_BATCH_PRUNE");
+        return e ? atoi(e) : 1;
+    }();
+    b.prune = batch_prune;
     rotor::launch_batch(b, n_slots, st);
     CK(cudaGetLastError());
     std::vector<double> h_c(P);

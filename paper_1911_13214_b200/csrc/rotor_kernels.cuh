@@ -27,8 +27,10 @@ struct BatchArgs {
     int *counter;               // work queue head, zeroed before the launch
     const int32_t *order;       // [n_problems] hand-out order of the queue (longest chains first)
     int mc;                     // m-chunk of the fill order (0: whole rows, diagonal by diagonal)
+    int prune;                  // 1/2/4: warp-group cells with the monotone-in-m candidate bound per 32/prune m (batch_cell_group); 0: wavefront_cell
 };
 size_t batch_slot_bytes(int L_max, int S);
+int batch_ctas_per_sm();  // k_batch's __launch_bounds__ residency: persistent CTAs per SM
 void launch_batch(const BatchArgs &b, int n_slots, cudaStream_t st);
 void launch_compact_ops(const rotor_op *src, const int64_t *src_off, const int64_t *cnt, const int64_t *dst_off,
                         rotor_op *dst, int P, cudaStream_t st);

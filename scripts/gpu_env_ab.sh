@@ -10,6 +10,6 @@ if [ "$K" != "-" ]; then
   echo "pytest rc=$? $(tail -1 $OUT/pytest_gpu.log)"; grep -E "^FAILED|Error" "$OUT/pytest_gpu.log" | head -5
 fi
 for rep in 1 2; do for v in $VALS; do
-  env $VAR=$v timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $OUT/bench_${v}_$rep.json 2> $OUT/bench_${v}_$rep.err
+  env $VAR=$v timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline ${BENCH_ARGS:-} > $OUT/bench_${v}_$rep.json 2> $OUT/bench_${v}_$rep.err
   echo "$VAR=$v $(grep -o '"ms_per_step": [0-9.]*' $OUT/bench_${v}_$rep.json | head -2 | tr '\n' ' ') $(grep -o '"middle_ms_per_step": [0-9.]*' $OUT/bench_${v}_$rep.json)"
 done; done

@@ -267,6 +267,19 @@ def test_monotone_config2(oracle_mod):
     assert np.array_equal(np.isinf(C), D == O.NONE)
 
 
+def test_monotone_in_m_every_cell_both_modes(oracle_mod):
+    """P4 for every cell of config-5-shaped tables in both modes (the property
+    k_batch's candidate bound rests on, DESIGN 5.3): C[s,t,m+1] <= C[s,t,m]
+    exactly, including the +inf prefix of each row."""
+    O = oracle_mod
+    chains, limits, S = G.config5(n_limits=3)
+    for ch, lims in zip(chains[:3], limits[:3]):
+        for restricted in (False, True):
+            o = O.OracleSolve(ch, lims[-1], S, restricted=restricted)
+            C, _ = o.tables()
+            assert np.all(C[:, 1:] <= C[:, :-1]), (ch.L, restricted)
+
+
 def test_unit_chain_first_feasible(oracle_mod):
     O = oracle_mod
     for L in range(1, 12):
