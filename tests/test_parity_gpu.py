@@ -579,3 +579,46 @@ def test_config5_all_costs_vs_oracle(R, oracle_mod, restricted):
                 assert bits(np.array([costs[i, j]])) == bits(np.array([c])), (i, j, costs[i, j], c)
                 if (i, j) in sample:
                     assert [tuple(map(int, r)) for r in ops[i * nl + j]] == o.reconstruct(), (i, j)
+
+
+_PRUNE_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, '.')
+import chaingen as G
+import paper_1911_13214_b200 as R
+chains, limits, S = G.config5(n_limits=12)
+for restricted in (False, True):
+    costs, status, n_ops, ops = R.solve_batch(chains, limits, S, with_ops=True, restricted=restricted)
+    print(int(restricted), ' '.join('%016x' % v for v in np.ascontiguousarray(costs).view(np.uint64).ravel()))
+    print(int(restricted), ' '.join(str(int(x)) for x in np.asarray(status).ravel()))
+    print(int(restricted), ' '.join(str(int(x)) for x in np.asarray(n_ops).ravel()))
+"""
+
+
+@pytest.mark.parametrize("mode", ["0", "2", "4"])
+def test_batch_prune_modes(R, oracle_mod, mode):
+    """The batch fill's alternative candidate paths (ROTOR_BATCH_PRUNE, read once
+    per process, so each runs in a subprocess): 0 = every candidate
+    (wavefront_cell), 2 / 4 = the monotone-in-m bound per 16 / 8 m.  Costs,
+    statuses and schedule lengths equal the default path's (bound per 32 m) in
+    both modes, and a sample of costs equals the oracle's."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for m in ("1", mode):
+        env = dict(os.environ, ROTOR_BATCH_PRUNE=m)
+        r = subprocess.run([sys.executable, "-c", _PRUNE_SCRIPT], cwd=root, env=env, capture_output=True,
+                           text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs[m] = r.stdout.split("\n")
+    assert outs["1"] == outs[mode]
+    O = oracle_mod
+    chains, limits, S = G.config5(n_limits=12)
+    first = outs[mode][0].split()[1:]
+    for i in range(0, len(chains), 3):
+        for j in (0, 5, 11):
+            c = O.OracleSolve(chains[i], limits[i][j], S, keep_d=False).cost
+            assert first[i * 12 + j] == "%016x" % int(bits(np.array([c]))[0])
