@@ -337,13 +337,32 @@ def solve_batch(chains, limits, slots: int, *, with_ops: bool = False, stream=No
                                _stream_ptr(stream), P(costs, _d), ops.ctypes.data if ops is not None else None,
                                P(offs, _i64), P(caps, _i64), P(n_ops, _i64), P(status, _i32))
     _check(r)
-    out_ops = None
-    if with_ops:
-        out_ops = []
-        for p in range(nc * nl):
-            k = int(n_ops.reshape(-1)[p])
-            out_ops.append(ops[offs[p]: offs[p] + max(k, 0)])  # views into one array
-    return costs, status, n_ops, out_ops
+    return costs, status, n_ops, (BatchOps(ops, offs, n_ops.reshape(-1)) if with_ops else None)
+
+
+class BatchOps:
+    """The schedules of a solve_batch call as a read-only sequence: item p (problem
+    chain p // n_limits, limit p % n_limits) is an [n_ops, 2] int32 view into one
+    array, made on access (no per-call Python loop over the problems)."""
+
+    def __init__(self, ops, offs, n_ops):
+        self._ops, self._offs, self._n = ops, offs, n_ops
+
+    def __len__(self):
+        return len(self._n)
+
+    def __getitem__(self, p):
+        if isinstance(p, slice):
+            return [self[i] for i in range(*p.indices(len(self)))]
+        if p < 0:
+            p += len(self)
+        if not 0 <= p < len(self):
+            raise IndexError(p)
+        o = int(self._offs[p])
+        return self._ops[o: o + max(int(self._n[p]), 0)]
+
+    def __iter__(self):
+        return (self[i] for i in range(len(self)))
 
 
 def solve_sharded(chain, mem_limit: int, slots: int, devices, *, halo_mode: int = 1, ops_cap: int | None = None,
