@@ -622,3 +622,28 @@ def test_batch_prune_modes(R, oracle_mod, mode):
         for j in (0, 5, 11):
             c = O.OracleSolve(chains[i], limits[i][j], S, keep_d=False).cost
             assert first[i * 12 + j] == "%016x" % int(bits(np.array([c]))[0])
+
+
+def test_batch_long_chains_several_bound_passes(R, oracle_mod):
+    """k_batch on chains long enough that a cell's candidates span several
+    32-candidate bound passes (t - s up to 150 > 64) and chains of mixed length
+    in one launch (ragged L_max padding), in both modes: every cost equals the
+    oracle's bit for bit, a sample of schedules equals its Algorithm 2."""
+    O = oracle_mod
+    chains = [G.long_chain(L=150, seed=21), G.block_chain("resnet", 70, seed=22), G.unit_chain(9)]
+    S = 120
+    nl = 5
+    limits = [[max(1, (i * G.budget_ref(c)) // (nl + 1)) for i in range(2, nl + 2)] for c in chains]
+    for restricted in (False, True):
+        costs, status, n_ops, ops = R.solve_batch(chains, limits, S, with_ops=True, restricted=restricted)
+        for i, ch in enumerate(chains):
+            for j in range(nl):
+                o = O.OracleSolve(ch, limits[i][j], S, restricted=restricted)
+                c = o.cost
+                if math.isinf(c):
+                    assert status[i, j] == R.INFEASIBLE and math.isinf(costs[i, j]), (i, j)
+                    continue
+                assert status[i, j] == R.OK, (i, j, status[i, j])
+                assert bits(np.array([costs[i, j]])) == bits(np.array([c])), (i, j, costs[i, j], c)
+                if j in (1, 4):
+                    assert [tuple(map(int, r)) for r in ops[i * nl + j]] == o.reconstruct(), (i, j)
